@@ -1,0 +1,209 @@
+/*
+ * tts.h -- C-ABI of libtts: the data-parallel hot path of one beam-search
+ * test-time-scaling (TTS) step on B200 (sm_100a).
+ *
+ * The method (arXiv 2509.00195, FlashTTS, section 3.1):
+ * each TTS step (1) extends every live beam by one "thinking step" of tokens
+ * -- a decode loop whose attention runs over a beam tree whose KV pages are
+ * shared by prefix -- then (2) a process reward model
+ * scores the beams and "the top-K candidates [are selected] globally with a
+ * static branching factor" and "replicated to spawn the next set of
+ * active beams".  Notation: N live beams per request, branching
+ * factor M, K = N / M survivors.
+ *
+ * Entry points and the passage each one implements:
+ *   tts_block_table_init_request  request install: all N beams start on the
+ *                                 shared prompt (SURVEY ledger C2, C6, C7)
+ *   tts_block_table_append        per-token KV append (Alg. 1 line 10
+ *                                 GenerateOneToken; ledger C7, C11, C12)
+ *   tts_prefix_attn_decode        prefix-shared decode attention over the beam
+ *                                 tree (P:148 paged attention, P:257-263 prefix
+ *                                 sharing, P:394 sibling grouping; ledger C10)
+ *   tts_beam_select_fork          Select + DuplicateThenTruncate without
+ *                                 truncation (Alg. 1 lines 15-19, P:345-347;
+ *                                 P:181; ledger C3-C8)
+ *   tts_block_table_release_request / _snapshot / _stats  lifecycle, debug
+ *                                 checkpoint, unique/logical KV accounting
+ *   tts_comm_init / tts_beam_select_fork_global  multi-GPU global top-K over
+ *                                 NCCL all-gather
+ *
+ * Memory ownership: the CALLER allocates every device buffer described by
+ * tts_buffers_t (sizes from tts_query_buffer_bytes) and keeps it alive and
+ * unmodified for the lifetime of the context.  libtts owns only its host-side
+ * context (and an NCCL communicator if tts_comm_init was called).  Buffers
+ * passed to individual calls (q, k/v, scores, out) are borrowed until the
+ * stream work of that call completes.
+ *
+ * Pointer convention: a parameter whose name ends in _h is HOST memory; every
+ * other pointer is DEVICE memory of the context's device.  All calls are
+ * stream-ordered on the given cudaStream_t (passed as void*); calls marked
+ * "syncs" synchronise that stream before returning.
+ *
+ * Errors: argument / shape / state errors detected on the host return a
+ * non-zero tts_status_t and enqueue nothing.  Data-dependent errors (page pool
+ * exhaustion) are recorded in the sticky device status word; every later
+ * kernel of the context becomes a no-op until tts_device_status reads and
+ * clears it, and the context state is then undefined (release and re-install
+ * the affected requests).  NaN / out-of-range scores are not errors (ledger C4).
+ *
+ * Threading: one context is driven by one host thread; no internal locking.
+ * Determinism: every integer output (survivors, parent maps, block tables,
+ * refcounts, free set) is a pure function of the call sequence (ledger C20).
+ */
+#ifndef TTS_H
+#define TTS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TTS_OK = 0,
+  TTS_ERR_INVALID_ARG = 1,   /* shape, range or N % M != 0      */
+  TTS_ERR_UNSUPPORTED = 2,   /* head_dim not in {64,128}, G > 16, ...       */
+  TTS_ERR_OUT_OF_PAGES = 3,  /* page pool exhausted (sticky device error)   */
+  TTS_ERR_CAPACITY = 4,      /* request id / beams / pages exceed config    */
+  TTS_ERR_STATE = 5,         /* request not installed / already installed   */
+  TTS_ERR_CUDA = 6,
+  TTS_ERR_NCCL = 7
+} tts_status_t;
+
+typedef struct tts_ctx* tts_ctx_t;
+
+/* Static shape of a context.  Page size P tokens; a page id indexes the same
+ * slot of every layer's K and V pool (ledger C9). */
+typedef struct {
+  int32_t num_layers;          /* L                                          */
+  int32_t num_q_heads;         /* Hq                                         */
+  int32_t num_kv_heads;        /* Hkv; G = Hq / Hkv consecutive q heads per kv head */
+  int32_t head_dim;            /* d in {64, 128}                             */
+  int32_t page_size;           /* P in {16} (tokens per page)                */
+  int32_t max_requests;        /* request ids are 0 .. max_requests-1        */
+  int32_t max_beams;           /* N_max (<= 1024); also the beam stride of q/out/k/v */
+  int32_t max_pages_per_beam;  /* table row length                           */
+  int64_t num_pages;           /* pool size                                  */
+} tts_config_t;
+
+/* Caller-owned device buffers (all sizes from tts_query_buffer_bytes). */
+typedef struct {
+  void* k_pool;            /* bf16 [L][num_pages][Hkv][P][d]  ("HND" pages) */
+  void* v_pool;            /* bf16 [L][num_pages][Hkv][P][d]                */
+  int32_t* block_tables;   /* [max_requests][max_beams][max_pages_per_beam] */
+  int32_t* seq_lens;       /* [max_requests][max_beams] tokens per beam     */
+  int32_t* refcounts;      /* [num_pages]                                   */
+  uint32_t* free_bitmap;   /* [ceil(num_pages/32)], bit = 1 means free      */
+  int32_t* status;         /* [4] sticky device status word                 */
+  void* workspace;         /* scratch, workspace_bytes                      */
+  size_t workspace_bytes;
+} tts_buffers_t;
+
+typedef struct {
+  size_t k_pool, v_pool, block_tables, seq_lens, refcounts, free_bitmap, status, workspace;
+} tts_buffer_sizes_t;
+
+/* Byte size of every caller-owned buffer for cfg.  Host only. */
+tts_status_t tts_query_buffer_bytes(const tts_config_t* cfg_h, tts_buffer_sizes_t* sizes_h);
+
+/* Create a context over caller-owned buffers on `device`; initialises the
+ * allocator state (all pages free, refcounts 0, status 0) with blocking
+ * device work on the default stream.  *out_h receives the handle. */
+tts_status_t tts_create(const tts_config_t* cfg_h, const tts_buffers_t* bufs_h, int device,
+                        tts_ctx_t* out_h);
+tts_status_t tts_destroy(tts_ctx_t ctx);
+const char* tts_status_str(tts_status_t s);
+
+/* Reads and clears the sticky device status word (syncs). */
+tts_status_t tts_device_status(tts_ctx_t ctx, void* stream, tts_status_t* out_h);
+
+/* Number of kernels this context has launched so far (host counter). */
+int64_t tts_launch_count(tts_ctx_t ctx);
+
+/* a1. Install request `req` with n_beams beams on a prompt of prompt_len
+ * tokens.  k_prompt / v_prompt: bf16 [L][prompt_len][Hkv][d].
+ * Allocates ceil(prompt_len/P) pages (lowest free ids, position order),
+ * points all beams' tables at them (refcount n_beams); a partial last prompt
+ * page is copied for beams 1..n_beams-1 (eager CoW, ledger C6).
+ * Errors: TTS_ERR_STATE if installed, TTS_ERR_CAPACITY if n_beams >
+ * max_beams or prompt pages > max_pages_per_beam. */
+tts_status_t tts_block_table_init_request(tts_ctx_t ctx, int32_t req, int32_t n_beams,
+                                          int32_t prompt_len, const void* k_prompt,
+                                          const void* v_prompt, void* stream);
+
+/* a2. Append one token to every active beam of the n_req requests req_ids_h
+ * (served in array order, beams ascending; ledger C7).  active_h: host uint8
+ * [n_req][max_beams] (NULL = all n_beams active).  k_new / v_new: bf16
+ * [L][n_req][max_beams][Hkv][d].  A beam with len % P == 0 first allocates
+ * the lowest free page.  Inactive beams are untouched (ledger C12). */
+tts_status_t tts_block_table_append(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
+                                    const uint8_t* active_h, const void* k_new,
+                                    const void* v_new, void* stream);
+
+/* a4+a5. Decode attention for layers [layer_begin, layer_end) of every active
+ * beam of the n_req requests, over all len tokens of the beam (the token just
+ * appended included; ledger C11):
+ *   out[l][i][b][h][:] = softmax_j(scale * q[l][i][b][h] . K_b[j][h/G]) V_b[j][h/G]
+ * q: bf16 [layer_end-layer_begin][n_req][max_beams][Hq][d];
+ * out: fp32, same shape; rows of inactive beams are not written.
+ * Each KV page shared by several beams of a request is read from HBM once
+ * per beam group and staged in shared memory for every beam and GQA head that
+ * references it (the cascade/tree decomposition). */
+tts_status_t tts_prefix_attn_decode(tts_ctx_t ctx, int32_t layer_begin, int32_t layer_end,
+                                    int32_t n_req, const int32_t* req_ids_h,
+                                    const uint8_t* active_h, const void* q,
+                                    float softmax_scale, float* out, void* stream);
+
+/* a2+a4 fused: tts_block_table_append then tts_prefix_attn_decode over all
+ * layers [0, L) in one call (one round of host planning, same kernels and
+ * semantics as the two calls in sequence).  Shapes as in those calls. */
+tts_status_t tts_decode_step(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
+                             const uint8_t* active_h, const void* k_new, const void* v_new,
+                             const void* q, float softmax_scale, float* out, void* stream);
+
+/* Live timing of the attention kernel: between tts_profile_begin and
+ * tts_profile_end every attention launch is bracketed by CUDA events recorded
+ * on its own stream; tts_profile_end syncs and returns the summed kernel time
+ * (ms) and the number of attention launches. */
+tts_status_t tts_profile_begin(tts_ctx_t ctx);
+tts_status_t tts_profile_end(tts_ctx_t ctx, double* attn_ms_h, int64_t* attn_launches_h);
+
+/* a6+a7. For each of the n_req requests (array order): select the K = N/M
+ * survivors by (score desc, index asc; NaN last, -0 == +0; ledger C3/C4),
+ * sort them by index, and fork child c = r*M + j from survivors[r] (ledger
+ * C5): rows and lengths copied, refcounts recounted, pages that drop to 0
+ * freed before any allocation, then eager CoW of partial last pages for
+ * children j >= 1 in (request, child) order (ledger C6, C7).
+ * scores: fp32 device [n_req][max_beams].  parent_out (nullable, device):
+ * int32 [n_req][max_beams] new -> old.  Errors: TTS_ERR_INVALID_ARG if
+ * N % M != 0.  Syncs (reads the parent map back for the host length mirror). */
+tts_status_t tts_beam_select_fork(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
+                                  const float* scores, int32_t width_m, int32_t* parent_out,
+                                  void* stream);
+
+/* Release every page of request `req` (refcount decrement, free at 0). */
+tts_status_t tts_block_table_release_request(tts_ctx_t ctx, int32_t req, void* stream);
+
+/* Debug checkpoint (syncs): tables_h int32 [n_beams][max_pages_per_beam],
+ * lens_h int32 [n_beams]; refcounts_h int32 [num_pages] and free_bitmap_h
+ * uint32 [ceil(num_pages/32)] are nullable.  n_beams_h receives N. */
+tts_status_t tts_block_table_snapshot(tts_ctx_t ctx, int32_t req, int32_t* n_beams_h,
+                                      int32_t* tables_h, int32_t* lens_h,
+                                      int32_t* refcounts_h, uint32_t* free_bitmap_h,
+                                      void* stream);
+
+/* KV accounting (ledger C22): adds to accum (device int64[2])
+ * [0] += unique valid tokens over the distinct pages touched by the active
+ * beams of the call, [1] += logical tokens (sum of active beams' len).
+ * Does not sync. */
+tts_status_t tts_block_table_stats(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
+                                   const uint8_t* active_h, int64_t* accum, void* stream);
+
+/* Host mirror of a request's beam lengths (no device access). */
+tts_status_t tts_seq_lens_host(tts_ctx_t ctx, int32_t req, int32_t* lens_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTS_H */

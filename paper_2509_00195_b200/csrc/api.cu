@@ -1,0 +1,499 @@
+// C-ABI entry points of libtts (include/tts.h): argument validation, the host
+// mirror of beam lengths, launch planning, workspace carving.  Every step of
+// the hot path runs in the kernels of block_table.cu / attention.cu.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "tts_internal.cuh"
+
+namespace tts {
+
+static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+static int64_t max_alloc_items(const tts_config_t& c) {
+  return (int64_t)c.max_requests * c.max_beams + c.max_pages_per_beam + c.max_beams;
+}
+
+size_t workspace_bytes(const tts_config_t& c) {
+  const size_t rows = (size_t)c.max_requests * c.max_beams;
+  size_t s = 0;
+  s += align_up(rows * c.max_pages_per_beam * 4);  // tmp tables
+  s += align_up(rows * 4);                          // tmp lens
+  s += align_up(rows * 4);                          // parent
+  s += align_up((size_t)max_alloc_items(c) * 4);   // page list
+  s += align_up((size_t)max_alloc_items(c) * sizeof(CowCopy));
+  s += align_up((size_t)c.num_pages * 4);           // stats marks
+  s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
+  return s;
+}
+
+void* upload(Ctx* c, const void* src, size_t bytes, cudaStream_t st, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (bytes > kUploadSlotBytes) {
+    *err = cudaErrorInvalidValue;
+    return nullptr;
+  }
+  const int slot = c->up_pos;
+  c->up_pos = (c->up_pos + 1) % kUploadSlots;
+  cudaEventSynchronize(c->ev[slot]);
+  uint8_t* h = c->pinned + (size_t)slot * kUploadSlotBytes;
+  uint8_t* d = c->ws_upload + (size_t)slot * kUploadSlotBytes;
+  std::memcpy(h, src, bytes);
+  *err = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
+  if (*err == cudaSuccess) *err = cudaEventRecord(c->ev[slot], st);
+  return d;
+}
+
+}  // namespace tts
+
+using tts::Ctx;
+
+struct tts_ctx : public Ctx {};
+
+static bool valid_cfg(const tts_config_t* c) {
+  if (!c) return false;
+  if (c->num_layers <= 0 || c->num_q_heads <= 0 || c->num_kv_heads <= 0) return false;
+  if (c->num_q_heads % c->num_kv_heads) return false;
+  if (c->page_size != 16) return false;
+  if (c->max_requests <= 0 || c->max_beams <= 0 || c->max_beams > 1024) return false;
+  if (c->max_pages_per_beam <= 0 || c->num_pages <= 0) return false;
+  return true;
+}
+
+extern "C" {
+
+const char* tts_status_str(tts_status_t s) {
+  switch (s) {
+    case TTS_OK: return "ok";
+    case TTS_ERR_INVALID_ARG: return "invalid argument";
+    case TTS_ERR_UNSUPPORTED: return "unsupported configuration";
+    case TTS_ERR_OUT_OF_PAGES: return "page pool exhausted";
+    case TTS_ERR_CAPACITY: return "capacity exceeded";
+    case TTS_ERR_STATE: return "invalid request state";
+    case TTS_ERR_CUDA: return "CUDA error";
+    case TTS_ERR_NCCL: return "NCCL error";
+  }
+  return "unknown";
+}
+
+tts_status_t tts_query_buffer_bytes(const tts_config_t* cfg, tts_buffer_sizes_t* s) {
+  if (!valid_cfg(cfg) || !s) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& c = *cfg;
+  const size_t pool = (size_t)c.num_layers * c.num_pages * c.num_kv_heads * c.page_size * c.head_dim * 2;
+  s->k_pool = pool;
+  s->v_pool = pool;
+  s->block_tables = (size_t)c.max_requests * c.max_beams * c.max_pages_per_beam * 4;
+  s->seq_lens = (size_t)c.max_requests * c.max_beams * 4;
+  s->refcounts = (size_t)c.num_pages * 4;
+  s->free_bitmap = (size_t)((c.num_pages + 31) / 32) * 4;
+  s->status = 16;
+  s->workspace = tts::workspace_bytes(c);
+  return TTS_OK;
+}
+
+tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int device,
+                        tts_ctx_t* out) {
+  if (!valid_cfg(cfg) || !bufs || !out) return TTS_ERR_INVALID_ARG;
+  if (cfg->head_dim != 64 && cfg->head_dim != 128) return TTS_ERR_UNSUPPORTED;
+  if (cfg->num_q_heads / cfg->num_kv_heads > 16) return TTS_ERR_UNSUPPORTED;
+  const int64_t rows = (int64_t)cfg->num_layers * cfg->num_pages * cfg->num_kv_heads * cfg->page_size;
+  if (rows >= (1ll << 31)) return TTS_ERR_CAPACITY;
+  if (bufs->workspace_bytes < tts::workspace_bytes(*cfg)) return TTS_ERR_INVALID_ARG;
+  if (!bufs->k_pool || !bufs->v_pool || !bufs->block_tables || !bufs->seq_lens ||
+      !bufs->refcounts || !bufs->free_bitmap || !bufs->status || !bufs->workspace)
+    return TTS_ERR_INVALID_ARG;
+  TTS_CUDA(cudaSetDevice(device));
+  tts_ctx* c = new (std::nothrow) tts_ctx();
+  if (!c) return TTS_ERR_CAPACITY;
+  c->cfg = *cfg;
+  c->buf = *bufs;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  c->n_beams.assign(cfg->max_requests, 0);
+  c->lens.assign((size_t)cfg->max_requests * cfg->max_beams, 0);
+  // carve workspace
+  uint8_t* w = (uint8_t*)bufs->workspace;
+  const size_t rws = (size_t)cfg->max_requests * cfg->max_beams;
+  c->ws_tmp_tables = (int32_t*)w;
+  w += tts::align_up(rws * cfg->max_pages_per_beam * 4);
+  c->ws_tmp_lens = (int32_t*)w;
+  w += tts::align_up(rws * 4);
+  c->ws_parent = (int32_t*)w;
+  w += tts::align_up(rws * 4);
+  c->max_alloc = tts::max_alloc_items(*cfg);
+  c->ws_pages = (int32_t*)w;
+  w += tts::align_up((size_t)c->max_alloc * 4);
+  c->ws_cow = (tts::CowCopy*)w;
+  w += tts::align_up((size_t)c->max_alloc * sizeof(tts::CowCopy));
+  c->ws_mark = (int32_t*)w;
+  w += tts::align_up((size_t)cfg->num_pages * 4);
+  c->ws_upload = w;
+  if (cudaMallocHost(&c->pinned, (size_t)tts::kUploadSlots * tts::kUploadSlotBytes) != cudaSuccess) {
+    delete c;
+    return TTS_ERR_CUDA;
+  }
+  for (int i = 0; i < tts::kUploadSlots; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  if (!tts::make_tensor_maps(c)) {
+    tts_destroy(c);
+    return TTS_ERR_CUDA;
+  }
+  if (tts::launch_init_state(c, 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+    tts_destroy(c);
+    return TTS_ERR_CUDA;
+  }
+  *out = c;
+  return TTS_OK;
+}
+
+tts_status_t tts_destroy(tts_ctx_t c) {
+  if (!c) return TTS_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  for (int i = 0; i < tts::kUploadSlots; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  for (auto& e : c->prof_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  delete c;
+  return TTS_OK;
+}
+
+int64_t tts_launch_count(tts_ctx_t c) { return c ? c->launches : -1; }
+
+tts_status_t tts_device_status(tts_ctx_t c, void* stream, tts_status_t* out) {
+  if (!c || !out) return TTS_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t v = 0;
+  TTS_CUDA(cudaMemcpyAsync(&v, c->buf.status, 4, cudaMemcpyDeviceToHost, st));
+  TTS_CUDA(cudaMemsetAsync(c->buf.status, 0, 16, st));
+  TTS_CUDA(cudaStreamSynchronize(st));
+  *out = (tts_status_t)v;
+  return TTS_OK;
+}
+
+static bool installed(tts_ctx_t c, int32_t req) {
+  return req >= 0 && req < c->cfg.max_requests && c->n_beams[req] > 0;
+}
+
+static int64_t entry_of(const tts_config_t& g, int req, int beam, int pos) {
+  return ((int64_t)req * g.max_beams + beam) * g.max_pages_per_beam + pos;
+}
+
+tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_beams,
+                                          int32_t prompt_len, const void* k_prompt,
+                                          const void* v_prompt, void* stream) {
+  if (!c) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  if (req < 0 || req >= g.max_requests) return TTS_ERR_CAPACITY;
+  if (c->n_beams[req] > 0) return TTS_ERR_STATE;
+  if (n_beams <= 0 || n_beams > g.max_beams || prompt_len < 0) return TTS_ERR_INVALID_ARG;
+  if (prompt_len > 0 && (!k_prompt || !v_prompt)) return TTS_ERR_INVALID_ARG;
+  const int P = g.page_size;
+  const int npg = (prompt_len + P - 1) / P;
+  if (npg > g.max_pages_per_beam) return TTS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  std::vector<tts::AllocItem> items;
+  for (int i = 0; i < npg; ++i) items.push_back({entry_of(g, req, 0, i), 0, 0});
+  if (!items.empty()) {
+    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_broadcast_prompt(c, req, n_beams, npg, st));
+    TTS_CUDA(tts::launch_write_prompt(c, req, prompt_len, (const __nv_bfloat16*)k_prompt,
+                                      (const __nv_bfloat16*)v_prompt, st));
+  }
+  const int rem = prompt_len % P;
+  if (rem && n_beams > 1) {
+    items.clear();
+    for (int b = 1; b < n_beams; ++b) items.push_back({entry_of(g, req, b, npg - 1), 1, rem});
+    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
+  }
+  std::vector<int32_t> lens(g.max_beams, 0);
+  for (int b = 0; b < n_beams; ++b) lens[b] = prompt_len;
+  void* d = tts::upload(c, lens.data(), lens.size() * 4, st, &e);
+  TTS_CUDA(e);
+  TTS_CUDA(cudaMemcpyAsync(c->buf.seq_lens + (int64_t)req * g.max_beams, d, lens.size() * 4,
+                           cudaMemcpyDeviceToDevice, st));
+  c->n_beams[req] = n_beams;
+  std::copy(lens.begin(), lens.end(), c->lens.begin() + (int64_t)req * g.max_beams);
+  return TTS_OK;
+}
+
+static tts_status_t append_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
+                                const uint8_t* active, const void* k_new, const void* v_new,
+                                void* stream) {
+  if (!c || n_req <= 0 || !req_ids || !k_new || !v_new) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
+  std::vector<tts::AllocItem> items;
+  std::vector<int32_t> slots;
+  for (int i = 0; i < n_req; ++i) {
+    const int r = req_ids[i];
+    if (!installed(c, r)) return TTS_ERR_STATE;
+    for (int b = 0; b < c->n_beams[r]; ++b) {
+      if (active && !active[(int64_t)i * g.max_beams + b]) continue;
+      const int pos = c->lens[(int64_t)r * g.max_beams + b];
+      if (pos / P >= g.max_pages_per_beam) return TTS_ERR_CAPACITY;
+      if (pos % P == 0) items.push_back({entry_of(g, r, b, pos / P), 0, 0});
+      slots.insert(slots.end(), {i, r, b, pos});
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (!items.empty()) {
+    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+  }
+  if (!slots.empty()) {
+    void* d = tts::upload(c, slots.data(), slots.size() * 4, st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_append_write(c, (const int32_t*)d, (int)slots.size() / 4, n_req,
+                                      (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
+  }
+  for (size_t k = 0; k < slots.size(); k += 4) c->lens[(int64_t)slots[k + 1] * g.max_beams + slots[k + 2]]++;
+  return TTS_OK;
+}
+
+tts_status_t tts_block_table_append(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
+                                    const uint8_t* active, const void* k_new, const void* v_new,
+                                    void* stream) {
+  return append_impl(c, n_req, req_ids, active, k_new, v_new, stream);
+}
+
+static void prof_pair(tts_ctx_t c, cudaEvent_t* e0, cudaEvent_t* e1);
+
+// Group plan: contiguous beam runs of `gb` slots with >= 1 active beam.
+static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const uint8_t* active,
+                        int gb, std::vector<tts::GroupDesc>& out) {
+  const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
+  out.clear();
+  for (int i = 0; i < n_req; ++i) {
+    const int r = req_ids[i];
+    const int N = c->n_beams[r];
+    for (int b0 = 0; b0 < N; b0 += gb) {
+      tts::GroupDesc d{};
+      d.call_idx = i;
+      d.req = r;
+      d.beam0 = b0;
+      d.nbeams = std::min(gb, N - b0);
+      d.active = 0;
+      d.max_npages = 0;
+      for (int k = 0; k < d.nbeams; ++k) {
+        if (active && !active[(int64_t)i * g.max_beams + b0 + k]) continue;
+        d.active |= 1u << k;
+        const int len = c->lens[(int64_t)r * g.max_beams + b0 + k];
+        d.max_npages = std::max(d.max_npages, (len + P - 1) / P);
+      }
+      if (d.active) out.push_back(d);
+    }
+  }
+}
+
+tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t layer_end,
+                                    int32_t n_req, const int32_t* req_ids, const uint8_t* active,
+                                    const void* q, float scale, float* out, void* stream) {
+  if (!c || !req_ids || !q || !out || n_req <= 0) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  if (layer_begin < 0 || layer_end > g.num_layers || layer_begin >= layer_end) return TTS_ERR_INVALID_ARG;
+  for (int i = 0; i < n_req; ++i)
+    if (!installed(c, req_ids[i])) return TTS_ERR_STATE;
+  const int G = g.num_q_heads / g.num_kv_heads;
+  const int bpt = 16 / G;
+  const int n_layers = layer_end - layer_begin;
+  int forced = 0;
+  if (const char* s = std::getenv("TTS_NCONS")) forced = std::atoi(s);
+  std::vector<tts::GroupDesc> groups;
+  int chosen = 0;
+  for (int ncons : {8, 4, 2, 1}) {
+    if (ncons * bpt > 32) continue;
+    if (forced && ncons != forced) continue;
+    plan_groups(c, n_req, req_ids, active, ncons * bpt, groups);
+    chosen = ncons;
+    const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
+    if (forced || ctas >= 2ll * c->num_sms) break;
+  }
+  if (!chosen) return TTS_ERR_UNSUPPORTED;
+  if (groups.empty()) return TTS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
+  TTS_CUDA(e);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) prof_pair(c, &e0, &e1);
+  if (e0) TTS_CUDA(cudaEventRecord(e0, st));
+  TTS_CUDA(tts::launch_attention(c, (const tts::GroupDesc*)d, (int)groups.size(), chosen * bpt,
+                                 layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out, st));
+  if (e1) TTS_CUDA(cudaEventRecord(e1, st));
+  return TTS_OK;
+}
+
+tts_status_t tts_decode_step(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
+                             const uint8_t* active, const void* k_new, const void* v_new,
+                             const void* q, float scale, float* out, void* stream) {
+  tts_status_t s = append_impl(c, n_req, req_ids, active, k_new, v_new, stream);
+  if (s != TTS_OK) return s;
+  return tts_prefix_attn_decode(c, 0, c->cfg.num_layers, n_req, req_ids, active, q, scale, out, stream);
+}
+
+static constexpr int kProfPairs = 4096;
+
+static void prof_drain(tts_ctx_t c, int pair) {
+  cudaEvent_t a = c->prof_ev[2 * pair], b = c->prof_ev[2 * pair + 1];
+  if (cudaEventSynchronize(b) == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) c->prof_ms += ms;
+  }
+}
+
+static void prof_pair(tts_ctx_t c, cudaEvent_t* e0, cudaEvent_t* e1) {
+  const int i = c->prof_pos;
+  if (c->prof_count >= kProfPairs) prof_drain(c, i);  // pair i is being reused
+  *e0 = c->prof_ev[2 * i];
+  *e1 = c->prof_ev[2 * i + 1];
+  c->prof_pos = (i + 1) % kProfPairs;
+  c->prof_count++;
+}
+
+tts_status_t tts_profile_begin(tts_ctx_t c) {
+  if (!c) return TTS_ERR_INVALID_ARG;
+  if (c->prof_ev.empty()) {
+    c->prof_ev.resize(2 * kProfPairs);
+    for (auto& e : c->prof_ev) TTS_CUDA(cudaEventCreate(&e));
+  }
+  c->profiling = true;
+  c->prof_pos = 0;
+  c->prof_count = 0;
+  c->prof_ms = 0.0;
+  return TTS_OK;
+}
+
+tts_status_t tts_profile_end(tts_ctx_t c, double* ms, int64_t* n) {
+  if (!c || !c->profiling) return TTS_ERR_STATE;
+  const int64_t live = c->prof_count < kProfPairs ? c->prof_count : kProfPairs;
+  for (int64_t k = 0; k < live; ++k) {
+    const int i = (int)((c->prof_pos - live + k + kProfPairs) % kProfPairs);
+    prof_drain(c, i);
+  }
+  c->profiling = false;
+  if (ms) *ms = c->prof_ms;
+  if (n) *n = c->prof_count;
+  return TTS_OK;
+}
+
+tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
+                                  const float* scores, int32_t M, int32_t* parent_out,
+                                  void* stream) {
+  if (!c || n_req <= 0 || !req_ids || !scores) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  for (int i = 0; i < n_req; ++i)
+    if (!installed(c, req_ids[i])) return TTS_ERR_STATE;
+  const int N = c->n_beams[req_ids[0]];
+  for (int i = 0; i < n_req; ++i)
+    if (c->n_beams[req_ids[i]] != N) return TTS_ERR_INVALID_ARG;
+  if (M <= 0 || N % M) return TTS_ERR_INVALID_ARG;
+  for (int i = 0; i < n_req; ++i)
+    for (int j = 0; j < i; ++j)
+      if (req_ids[i] == req_ids[j]) return TTS_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  void* dreq = tts::upload(c, req_ids, (size_t)n_req * 4, st, &e);
+  TTS_CUDA(e);
+  TTS_CUDA(tts::launch_select(c, (const int32_t*)dreq, n_req, scores, N, M, parent_out, st));
+  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, n_req, N, st));
+  // parent map back to the host (for the length mirror and the CoW plan)
+  std::vector<int32_t> parent((size_t)n_req * g.max_beams);
+  TTS_CUDA(cudaMemcpyAsync(parent.data(), c->ws_parent, parent.size() * 4, cudaMemcpyDeviceToHost, st));
+  TTS_CUDA(cudaStreamSynchronize(st));
+  const int P = g.page_size;
+  std::vector<tts::AllocItem> items;
+  for (int i = 0; i < n_req; ++i) {
+    const int r = req_ids[i];
+    int32_t* lens = c->lens.data() + (int64_t)r * g.max_beams;
+    std::vector<int32_t> old(lens, lens + N);
+    for (int cc = 0; cc < N; ++cc) {
+      const int par = parent[(int64_t)i * g.max_beams + cc];
+      if (par < 0 || par >= N) return TTS_ERR_STATE;  // sticky device error upstream
+      lens[cc] = old[par];
+    }
+    for (int cc = 0; cc < N; ++cc) {
+      const int len = lens[cc];
+      if (cc % M >= 1 && len % P) items.push_back({entry_of(g, r, cc, (len - 1) / P), 1, len % P});
+    }
+  }
+  if (!items.empty()) {
+    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
+  }
+  return TTS_OK;
+}
+
+tts_status_t tts_block_table_release_request(tts_ctx_t c, int32_t req, void* stream) {
+  if (!c) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  TTS_CUDA(tts::launch_release(c, req, c->n_beams[req], (cudaStream_t)stream));
+  c->n_beams[req] = 0;
+  std::fill(c->lens.begin() + (int64_t)req * c->cfg.max_beams,
+            c->lens.begin() + (int64_t)(req + 1) * c->cfg.max_beams, 0);
+  return TTS_OK;
+}
+
+tts_status_t tts_block_table_snapshot(tts_ctx_t c, int32_t req, int32_t* n_beams_h,
+                                      int32_t* tables_h, int32_t* lens_h, int32_t* ref_h,
+                                      uint32_t* bitmap_h, void* stream) {
+  if (!c || !tables_h || !lens_h) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  const tts_config_t& g = c->cfg;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = c->n_beams[req];
+  if (n_beams_h) *n_beams_h = N;
+  TTS_CUDA(cudaMemcpyAsync(tables_h, c->buf.block_tables + entry_of(g, req, 0, 0),
+                           (size_t)N * g.max_pages_per_beam * 4, cudaMemcpyDeviceToHost, st));
+  TTS_CUDA(cudaMemcpyAsync(lens_h, c->buf.seq_lens + (int64_t)req * g.max_beams, (size_t)N * 4,
+                           cudaMemcpyDeviceToHost, st));
+  if (ref_h)
+    TTS_CUDA(cudaMemcpyAsync(ref_h, c->buf.refcounts, (size_t)g.num_pages * 4, cudaMemcpyDeviceToHost, st));
+  if (bitmap_h)
+    TTS_CUDA(cudaMemcpyAsync(bitmap_h, c->buf.free_bitmap, (size_t)((g.num_pages + 31) / 32) * 4,
+                             cudaMemcpyDeviceToHost, st));
+  TTS_CUDA(cudaStreamSynchronize(st));
+  return TTS_OK;
+}
+
+tts_status_t tts_block_table_stats(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
+                                   const uint8_t* active, int64_t* accum, void* stream) {
+  if (!c || n_req <= 0 || !req_ids || !accum) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  for (int i = 0; i < n_req; ++i)
+    if (!installed(c, req_ids[i])) return TTS_ERR_STATE;
+  std::vector<tts::GroupDesc> groups;
+  plan_groups(c, n_req, req_ids, active, 32, groups);
+  int64_t logical = 0;
+  for (const auto& d : groups)
+    for (int k = 0; k < d.nbeams; ++k)
+      if ((d.active >> k) & 1u) logical += c->lens[(int64_t)d.req * g.max_beams + d.beam0 + k];
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  void* d = groups.empty() ? nullptr
+                           : tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
+  if (!groups.empty()) TTS_CUDA(e);
+  TTS_CUDA(tts::launch_stats(c, (const tts::GroupDesc*)d, (int)groups.size(), accum, logical, st));
+  return TTS_OK;
+}
+
+tts_status_t tts_seq_lens_host(tts_ctx_t c, int32_t req, int32_t* lens_h) {
+  if (!c || !lens_h) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  std::memcpy(lens_h, c->lens.data() + (int64_t)req * c->cfg.max_beams, (size_t)c->n_beams[req] * 4);
+  return TTS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Internal declarations of libtts (not part of the C-ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/tts.h"
+
+#define TTS_CUDA(call)                                      \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return TTS_ERR_CUDA;             \
+  } while (0)
+
+namespace tts {
+
+constexpr int kUploadSlots = 64;
+constexpr size_t kUploadSlotBytes = 256 * 1024;
+
+// One CTA group of the attention kernel: a contiguous run of beams of one
+// request (DFS order, so every shared page's beams form a sub-run).
+struct GroupDesc {
+  int32_t call_idx;    // index of the request in the call (q/out stride)
+  int32_t req;         // request id
+  int32_t beam0;       // first beam slot
+  int32_t nbeams;      // beams in the group (<= 32)
+  uint32_t active;     // bit i: beam0 + i active
+  int32_t max_npages;  // max over active beams of ceil(len / P)
+  int32_t pad[2];
+};
+
+// Allocation item: table entry to receive a fresh page.
+struct AllocItem {
+  int64_t entry;  // flat index into block_tables
+  int32_t cow;    // 1: old entry value is a CoW source (ref -1, copy recorded)
+  int32_t ntok;   // tokens to copy when cow
+};
+
+struct CowCopy {
+  int32_t src, dst, ntok, pad;
+};
+
+struct Ctx {
+  tts_config_t cfg;
+  tts_buffers_t buf;
+  int device = 0;
+  int num_sms = 148;
+  int64_t launches = 0;
+  // host mirror of lengths / beam counts (lengths change only through the API)
+  std::vector<int32_t> n_beams;  // per request, 0 = not installed
+  std::vector<int32_t> lens;     // [max_requests][max_beams]
+  // pinned upload ring
+  uint8_t* pinned = nullptr;
+  cudaEvent_t ev[kUploadSlots];
+  int up_pos = 0;
+  // workspace carve (device)
+  int32_t* ws_tmp_tables = nullptr;  // [max_requests * max_beams * max_pages]
+  int32_t* ws_tmp_lens = nullptr;    // [max_requests * max_beams]
+  int32_t* ws_parent = nullptr;      // [max_requests * max_beams]
+  int32_t* ws_pages = nullptr;       // allocator output list
+  CowCopy* ws_cow = nullptr;         // [max_alloc]
+  int32_t* ws_mark = nullptr;        // [num_pages] (stats)
+  uint8_t* ws_upload = nullptr;      // device mirror of the upload ring
+  int64_t max_alloc = 0;
+  // live attention timing (tts_profile_begin/_end)
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  int prof_pos = 0;
+  int64_t prof_count = 0;
+  double prof_ms = 0.0;
+  // TMA descriptors (K / V pools, 2D view [rows][d])
+  CUtensorMap tmap_k, tmap_v;
+  bool tmap_ok = false;
+};
+
+// Device-copy a host blob through the pinned ring; returns device pointer.
+void* upload(Ctx* c, const void* src, size_t bytes, cudaStream_t s, cudaError_t* err);
+
+size_t workspace_bytes(const tts_config_t& cfg);
+
+// kernels (block_table.cu)
+cudaError_t launch_init_state(Ctx* c, cudaStream_t s);
+cudaError_t launch_alloc(Ctx* c, const AllocItem* items_d, int n_items, cudaStream_t s);
+cudaError_t launch_broadcast_prompt(Ctx* c, int req, int n_beams, int npg, cudaStream_t s);
+cudaError_t launch_write_prompt(Ctx* c, int req, int prompt_len, const __nv_bfloat16* k,
+                                const __nv_bfloat16* v, cudaStream_t s);
+cudaError_t launch_cow_copy(Ctx* c, int n_items, cudaStream_t s);
+cudaError_t launch_append_write(Ctx* c, const int32_t* slots_d, int n_slots, int n_req,
+                                const __nv_bfloat16* k, const __nv_bfloat16* v, cudaStream_t s);
+cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float* scores,
+                          int N, int M, int32_t* parent_out, cudaStream_t s);
+cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int N, cudaStream_t s);
+cudaError_t launch_release(Ctx* c, int req, int n_beams, cudaStream_t s);
+cudaError_t launch_stats(Ctx* c, const GroupDesc* groups_d, int n_groups, int64_t* accum,
+                         int64_t logical, cudaStream_t s);
+
+// attention.cu
+cudaError_t launch_attention(Ctx* c, const GroupDesc* groups_d, int n_groups, int group_beams,
+                             int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
+                             float scale, float* out, cudaStream_t s);
+bool make_tensor_maps(Ctx* c);
+
+}  // namespace tts

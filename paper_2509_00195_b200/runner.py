@@ -1,0 +1,127 @@
+"""Driver of the beam-step hot path through the C-ABI (the call sequence a
+serving loop makes): install every request on its prompt, then per decode
+iteration append + prefix-shared attention for all layers, and at each step
+end select + fork (PAPER.md 3.1 two-stage loop; Alg. 1 lines 7-19).
+
+Inputs are the seeded synthetic tensors of ``synth`` generated directly on the
+device (input generation is not part of the method and is excluded from any
+timed region by the callers).  Nothing here computes the method: every step
+runs in libtts's kernels.
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from synth import rng, workload
+from .tts import Context, TTSConfig
+
+
+def tts_config(cfg: workload.Config, n_req: int, num_pages: Optional[int] = None,
+               max_pages_per_beam: Optional[int] = None) -> TTSConfig:
+    mp = max_pages_per_beam or workload.max_pages_per_beam(cfg)
+    if num_pages is None:
+        num_pages = cfg.num_pages or (n_req * cfg.N * mp + 64)
+    return TTSConfig(num_layers=cfg.L, num_q_heads=cfg.Hq, num_kv_heads=cfg.Hkv, head_dim=cfg.d,
+                     page_size=cfg.P, max_requests=n_req, max_beams=cfg.N, max_pages_per_beam=mp,
+                     num_pages=int(num_pages))
+
+
+class Inputs:
+    """Identity-keyed synthetic q / k / v / scores on the device."""
+
+    def __init__(self, cfg: workload.Config, device):
+        self.cfg = cfg
+        self.dev = device
+
+    def _idx(self, n, shape_pos, ndim):
+        s = [1] * ndim
+        s[shape_pos] = n
+        return torch.arange(n, device=self.dev).view(*s)
+
+    def prompt_kv(self, req: int):
+        c = self.cfg
+        l = self._idx(c.L, 0, 3)
+        pos = self._idx(c.prompt, 1, 3)
+        h = self._idx(c.Hkv, 2, 3)
+        k = rng.kv_prompt_values(c.seed, "k", l, req, pos, h, c.d, device=self.dev)
+        v = rng.kv_prompt_values(c.seed, "v", l, req, pos, h, c.d, device=self.dev)
+        return k.contiguous(), v.contiguous()
+
+    def step(self, t: int, greqs: Sequence[int]):
+        """q [L][n][N][Hq][d], k/v [L][n][N][Hkv][d] for global requests greqs."""
+        c = self.cfg
+        l = self._idx(c.L, 0, 4)
+        r = torch.tensor(list(greqs), device=self.dev).view(1, -1, 1, 1)
+        b = self._idx(c.N, 2, 4)
+        hq = self._idx(c.Hq, 3, 4)
+        hk = self._idx(c.Hkv, 3, 4)
+        q = rng.q_values(c.seed, l, r, t, b, hq, c.d, c.q_scale, device=self.dev)
+        k = rng.kv_decode_values(c.seed, "k", l, r, t, b, hk, c.d, device=self.dev)
+        v = rng.kv_decode_values(c.seed, "v", l, r, t, b, hk, c.d, device=self.dev)
+        return q.contiguous(), k.contiguous(), v.contiguous()
+
+    def scores(self, greq: int, step: int):
+        return workload.scores(self.cfg, greq, step, device=self.dev)
+
+
+class BeamStepRunner:
+    def __init__(self, cfg: workload.Config, req_ids: Optional[Sequence[int]] = None, device: int = 0,
+                 num_pages: Optional[int] = None, fused: bool = True):
+        self.cfg = cfg
+        self.fused = fused
+        self.req_ids = list(range(cfg.R)) if req_ids is None else list(req_ids)
+        self.local = {r: i for i, r in enumerate(self.req_ids)}
+        self.tcfg = tts_config(cfg, len(self.req_ids), num_pages)
+        self.ctx = Context(self.tcfg, device)
+        self.dev = self.ctx.device
+        self.inputs = Inputs(cfg, self.dev)
+        self.scale = 1.0 / math.sqrt(cfg.d)
+
+    def install(self):
+        for r in self.req_ids:
+            k, v = self.inputs.prompt_kv(r)
+            self.ctx.tts_block_table_init_request(self.local[r], self.cfg.N, self.cfg.prompt, k, v)
+
+    def release(self):
+        for r in self.req_ids:
+            self.ctx.tts_block_table_release_request(self.local[r])
+
+    def run(self, on_iter: Optional[Callable] = None, on_fork: Optional[Callable] = None,
+            max_iters: Optional[int] = None, scores_fn: Optional[Callable] = None) -> int:
+        """Whole run; returns beam-steps.  on_iter(it, out, q) after attention;
+        on_fork(it, parents {greq: np.ndarray}) after each fork."""
+        c = self.cfg
+        self.install()
+        beam_steps = 0
+        for it in workload.schedule(c, self.req_ids):
+            if max_iters is not None and it.t >= max_iters:
+                break
+            n = len(it.reqs)
+            loc = [self.local[r] for r in it.reqs]
+            active = np.stack(it.active).astype(np.uint8)
+            q, k, v = self.inputs.step(it.t, it.reqs)
+            out = torch.empty(c.L, n, c.N, c.Hq, c.d, dtype=torch.float32, device=self.dev)
+            if self.fused:
+                self.ctx.tts_decode_step(loc, active, k, v, q, self.scale, out)
+            else:
+                self.ctx.tts_block_table_append(loc, active, k, v)
+                self.ctx.tts_prefix_attn_decode(0, c.L, loc, active, q, self.scale, out)
+            beam_steps += int(active.sum())
+            if on_iter is not None:
+                on_iter(it, out, active)
+            if it.forks:
+                greqs = [r for r, _ in it.forks]
+                if scores_fn is not None:
+                    sc = torch.stack([torch.as_tensor(scores_fn(r, s), dtype=torch.float32)
+                                      for r, s in it.forks]).to(self.dev)
+                else:
+                    sc = torch.stack([self.inputs.scores(r, s) for r, s in it.forks])
+                parent = torch.empty(len(greqs), c.N, dtype=torch.int32, device=self.dev)
+                self.ctx.tts_beam_select_fork([self.local[r] for r in greqs], sc.contiguous(), c.M, parent)
+                if on_fork is not None:
+                    on_fork(it, {r: parent[i].cpu().numpy() for i, r in enumerate(greqs)})
+        return beam_steps

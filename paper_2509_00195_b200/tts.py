@@ -1,0 +1,277 @@
+"""Thin ctypes binding of libtts (include/tts.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA kernels behind the C-ABI.  The
+functions carry the C names; ``Context`` owns the caller-side device buffers.
+
+There is no fallback: if libtts.so is missing or no CUDA device is present,
+constructing a Context raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtts.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "tts.h")
+
+
+class TTSError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        super().__init__(f"{what}: libtts status {code} ({status_str(code)})")
+
+
+class tts_config_t(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("max_requests", ctypes.c_int32),
+                ("max_beams", ctypes.c_int32), ("max_pages_per_beam", ctypes.c_int32),
+                ("num_pages", ctypes.c_int64)]
+
+
+class tts_buffers_t(ctypes.Structure):
+    _fields_ = [("k_pool", ctypes.c_void_p), ("v_pool", ctypes.c_void_p),
+                ("block_tables", ctypes.c_void_p), ("seq_lens", ctypes.c_void_p),
+                ("refcounts", ctypes.c_void_p), ("free_bitmap", ctypes.c_void_p),
+                ("status", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t)]
+
+
+class tts_buffer_sizes_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_size_t) for n in ("k_pool", "v_pool", "block_tables", "seq_lens",
+                                               "refcounts", "free_bitmap", "status", "workspace")]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_2509_00195_b200.build` "
+                               "or __graft_entry__.build()")
+        lib = ctypes.CDLL(LIB_PATH)
+        sig = {
+            "tts_query_buffer_bytes": [ctypes.POINTER(tts_config_t), ctypes.POINTER(tts_buffer_sizes_t)],
+            "tts_create": [ctypes.POINTER(tts_config_t), ctypes.POINTER(tts_buffers_t), ctypes.c_int, ctypes.POINTER(_P)],
+            "tts_destroy": [_P],
+            "tts_device_status": [_P, _P, ctypes.POINTER(ctypes.c_int)],
+            "tts_block_table_init_request": [_P, _I, _I, _I, _P, _P, _P],
+            "tts_block_table_append": [_P, _I, _P, _P, _P, _P, _P],
+            "tts_prefix_attn_decode": [_P, _I, _I, _I, _P, _P, _P, ctypes.c_float, _P, _P],
+            "tts_beam_select_fork": [_P, _I, _P, _P, _I, _P, _P],
+            "tts_block_table_release_request": [_P, _I, _P],
+            "tts_block_table_snapshot": [_P, _I, _P, _P, _P, _P, _P, _P],
+            "tts_block_table_stats": [_P, _I, _P, _P, _P, _P],
+            "tts_seq_lens_host": [_P, _I, _P],
+            "tts_decode_step": [_P, _I, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P],
+            "tts_profile_begin": [_P],
+            "tts_profile_end": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)],
+        }
+        for name, args in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        lib.tts_status_str.argtypes = [ctypes.c_int]
+        lib.tts_status_str.restype = ctypes.c_char_p
+        lib.tts_launch_count.argtypes = [_P]
+        lib.tts_launch_count.restype = ctypes.c_int64
+        _lib = lib
+    return _lib
+
+
+def header_functions() -> list:
+    """Function names declared in include/tts.h (for the export test)."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tts_[a-z0-9_]+)\s*\(", src)))
+
+
+def status_str(code: int) -> str:
+    try:
+        return load().tts_status_str(code).decode()
+    except Exception:
+        return "?"
+
+
+def _check(code: int, what: str) -> None:
+    if code != 0:
+        raise TTSError(code, what)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _i32_host(xs: Sequence[int]):
+    a = (ctypes.c_int32 * len(xs))(*[int(x) for x in xs])
+    return a
+
+
+def _u8_host(active: Optional[np.ndarray]):
+    if active is None:
+        return None, None
+    a = np.ascontiguousarray(active, dtype=np.uint8)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+@dataclass
+class TTSConfig:
+    num_layers: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int
+    page_size: int
+    max_requests: int
+    max_beams: int
+    max_pages_per_beam: int
+    num_pages: int
+
+    def c(self) -> tts_config_t:
+        return tts_config_t(self.num_layers, self.num_q_heads, self.num_kv_heads, self.head_dim,
+                            self.page_size, self.max_requests, self.max_beams,
+                            self.max_pages_per_beam, self.num_pages)
+
+
+def query_buffer_bytes(cfg: TTSConfig) -> dict:
+    s = tts_buffer_sizes_t()
+    c = cfg.c()
+    _check(load().tts_query_buffer_bytes(ctypes.byref(c), ctypes.byref(s)), "tts_query_buffer_bytes")
+    return {n: getattr(s, n) for n, _ in tts_buffer_sizes_t._fields_}
+
+
+class Context:
+    """Owns the caller-side device buffers (torch) and the libtts context."""
+
+    def __init__(self, cfg: TTSConfig, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libtts needs a CUDA device (no CPU fallback)")
+        lib = load()
+        self.lib = lib
+        self.cfg = cfg
+        self.device = torch.device("cuda", device)
+        sz = query_buffer_bytes(cfg)
+        dev = self.device
+
+        def buf(n, dtype=torch.uint8):
+            return torch.empty(max(int(n), 16) // torch.tensor([], dtype=dtype).element_size(),
+                               dtype=dtype, device=dev)
+
+        self.k_pool = buf(sz["k_pool"], torch.bfloat16)
+        self.v_pool = buf(sz["v_pool"], torch.bfloat16)
+        self.block_tables = buf(sz["block_tables"], torch.int32)
+        self.seq_lens = buf(sz["seq_lens"], torch.int32)
+        self.refcounts = buf(sz["refcounts"], torch.int32)
+        self.free_bitmap = buf(sz["free_bitmap"], torch.int32)
+        self.status = buf(sz["status"], torch.int32)
+        self.workspace = buf(sz["workspace"], torch.uint8)
+        b = tts_buffers_t(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.block_tables.data_ptr(),
+                          self.seq_lens.data_ptr(), self.refcounts.data_ptr(),
+                          self.free_bitmap.data_ptr(), self.status.data_ptr(),
+                          self.workspace.data_ptr(), self.workspace.numel())
+        h = ctypes.c_void_p()
+        c = cfg.c()
+        torch.cuda.synchronize(dev)
+        _check(lib.tts_create(ctypes.byref(c), ctypes.byref(b), device, ctypes.byref(h)), "tts_create")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.tts_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def launch_count(self) -> int:
+        return int(self.lib.tts_launch_count(self.h))
+
+    # -- C entry points (same names) ------------------------------------------
+    def tts_block_table_init_request(self, req, n_beams, prompt_len, k_prompt, v_prompt):
+        _check(self.lib.tts_block_table_init_request(self.h, req, n_beams, prompt_len, _ptr(k_prompt),
+                                                     _ptr(v_prompt), self.stream),
+               "tts_block_table_init_request")
+
+    def tts_block_table_append(self, req_ids, active, k_new, v_new):
+        _a, ap = _u8_host(active)
+        _check(self.lib.tts_block_table_append(self.h, len(req_ids), _i32_host(req_ids), ap,
+                                               _ptr(k_new), _ptr(v_new), self.stream),
+               "tts_block_table_append")
+
+    def tts_prefix_attn_decode(self, layer_begin, layer_end, req_ids, active, q, scale, out):
+        _a, ap = _u8_host(active)
+        _check(self.lib.tts_prefix_attn_decode(self.h, layer_begin, layer_end, len(req_ids),
+                                               _i32_host(req_ids), ap, _ptr(q), float(scale),
+                                               _ptr(out), self.stream),
+               "tts_prefix_attn_decode")
+
+    def tts_decode_step(self, req_ids, active, k_new, v_new, q, scale, out):
+        _a, ap = _u8_host(active)
+        _check(self.lib.tts_decode_step(self.h, len(req_ids), _i32_host(req_ids), ap, _ptr(k_new),
+                                        _ptr(v_new), _ptr(q), float(scale), _ptr(out), self.stream),
+               "tts_decode_step")
+
+    def tts_profile_begin(self):
+        _check(self.lib.tts_profile_begin(self.h), "tts_profile_begin")
+
+    def tts_profile_end(self):
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        _check(self.lib.tts_profile_end(self.h, ctypes.byref(ms), ctypes.byref(n)), "tts_profile_end")
+        return ms.value, n.value
+
+    def tts_beam_select_fork(self, req_ids, scores, width_m, parent_out=None):
+        _check(self.lib.tts_beam_select_fork(self.h, len(req_ids), _i32_host(req_ids), _ptr(scores),
+                                             int(width_m), _ptr(parent_out), self.stream),
+               "tts_beam_select_fork")
+
+    def tts_block_table_release_request(self, req):
+        _check(self.lib.tts_block_table_release_request(self.h, req, self.stream),
+               "tts_block_table_release_request")
+
+    def tts_block_table_snapshot(self, req, with_pool_state=True):
+        c = self.cfg
+        n = ctypes.c_int32()
+        tables = np.empty((c.max_beams, c.max_pages_per_beam), dtype=np.int32)
+        lens = np.empty(c.max_beams, dtype=np.int32)
+        ref = np.empty(c.num_pages, dtype=np.int32) if with_pool_state else None
+        bm = np.empty((c.num_pages + 31) // 32, dtype=np.uint32) if with_pool_state else None
+        _check(self.lib.tts_block_table_snapshot(
+            self.h, req, ctypes.byref(n), tables.ctypes.data_as(_P), lens.ctypes.data_as(_P),
+            None if ref is None else ref.ctypes.data_as(_P), None if bm is None else bm.ctypes.data_as(_P),
+            self.stream), "tts_block_table_snapshot")
+        N = n.value
+        out = {"n_beams": N, "tables": tables[:N], "lens": lens[:N]}
+        if with_pool_state:
+            out["ref"] = ref
+            bits = np.unpackbits(bm.view(np.uint8), bitorder="little")[: c.num_pages]
+            out["free"] = np.nonzero(bits)[0]
+        return out
+
+    def tts_block_table_stats(self, req_ids, active, accum):
+        _a, ap = _u8_host(active)
+        _check(self.lib.tts_block_table_stats(self.h, len(req_ids), _i32_host(req_ids), ap, _ptr(accum),
+                                              self.stream), "tts_block_table_stats")
+
+    def tts_device_status(self) -> int:
+        v = ctypes.c_int()
+        _check(self.lib.tts_device_status(self.h, self.stream, ctypes.byref(v)), "tts_device_status")
+        return v.value
+
+    def tts_seq_lens_host(self, req) -> np.ndarray:
+        out = np.empty(self.cfg.max_beams, dtype=np.int32)
+        _check(self.lib.tts_seq_lens_host(self.h, req, out.ctypes.data_as(_P)), "tts_seq_lens_host")
+        return out
