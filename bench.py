@@ -318,6 +318,7 @@ def main():
         greqs = [r for r in range(cfg.R) if r % ws == rank]
         scaling = "strong"
     else:
+        cfg = cfg.with_(R=rot * ws)  # independent requests of the same shape, rot per rank
         greqs = [rank * rot + i for i in range(rot)]
         scaling = "weak"
     b = Bench(cfg, greqs, local)

@@ -305,11 +305,42 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
   for (int i = 0; i < n_req; ++i)
     if (!installed(c, req_ids[i])) return TTS_ERR_STATE;
   const int G = g.num_q_heads / g.num_kv_heads;
-  const int bpt = 16 / G;
   const int n_layers = layer_end - layer_begin;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  const char* path = std::getenv("TTS_ATTN");
+  const bool use_umma = tts::umma_supported(c) && !(path && std::strcmp(path, "mma") == 0);
+  std::vector<tts::GroupDesc> groups;
+  if (use_umma) {
+    // 128-row tiles: balanced runs of <= floor(128/G) beams; positions split
+    // across a cluster when the grid would not fill the GPU
+    const int maxb = tts::umma_max_beams(c);
+    int gb = 1;
+    for (int i = 0; i < n_req; ++i) {
+      const int N = c->n_beams[req_ids[i]];
+      const int ng = (N + maxb - 1) / maxb;
+      gb = std::max(gb, (N + ng - 1) / ng);
+    }
+    plan_groups(c, n_req, req_ids, active, gb, groups);
+    if (groups.empty()) return TTS_OK;
+    const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
+    int splits = 1;
+    if (const char* s = std::getenv("TTS_SPLITS")) splits = std::max(1, std::min(8, std::atoi(s)));
+    else
+      while (splits < 8 && ctas * splits < 2ll * c->num_sms) splits *= 2;
+    void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
+    TTS_CUDA(e);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) prof_pair(c, &e0, &e1);
+    if (e0) TTS_CUDA(cudaEventRecord(e0, st));
+    TTS_CUDA(tts::launch_attention_umma(c, (const tts::GroupDesc*)d, (int)groups.size(), splits, layer_begin,
+                                        n_layers, n_req, (const __nv_bfloat16*)q, scale, out, st));
+    if (e1) TTS_CUDA(cudaEventRecord(e1, st));
+    return TTS_OK;
+  }
+  const int bpt = 16 / G;
   int forced = 0;
   if (const char* s = std::getenv("TTS_NCONS")) forced = std::atoi(s);
-  std::vector<tts::GroupDesc> groups;
   int chosen = 0;
   for (int ncons : {8, 4, 2, 1}) {
     if (ncons * bpt > 32) continue;
@@ -321,8 +352,6 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
   }
   if (!chosen) return TTS_ERR_UNSUPPORTED;
   if (groups.empty()) return TTS_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e;
   void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
   TTS_CUDA(e);
   cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "../../include/tts.h"
@@ -103,5 +104,11 @@ cudaError_t launch_attention(Ctx* c, const GroupDesc* groups_d, int n_groups, in
                              int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
                              float scale, float* out, cudaStream_t s);
 bool make_tensor_maps(Ctx* c);
+// attention_umma.cu (tcgen05 path: d = 128, 4 <= G <= 16)
+bool umma_supported(const Ctx* c);
+int umma_max_beams(const Ctx* c);
+cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_groups, int splits,
+                                  int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
+                                  float scale, float* out, cudaStream_t s);
 
 }  // namespace tts
