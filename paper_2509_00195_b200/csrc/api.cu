@@ -2,6 +2,7 @@
 // mirror of beam lengths, launch planning, workspace carving.  Every step of
 // the hot path runs in the kernels of block_table.cu / attention.cu.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -25,6 +26,8 @@ size_t workspace_bytes(const tts_config_t& c) {
   s += align_up((size_t)max_alloc_items(c) * 4);   // page list
   s += align_up((size_t)max_alloc_items(c) * sizeof(CowCopy));
   s += align_up((size_t)c.num_pages * 4);           // stats marks
+  s += align_up(rows * c.max_pages_per_beam * 16);  // attention plan items
+  s += align_up(rows * 4);                          // plan counts
   s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
   return s;
 }
@@ -129,6 +132,10 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   w += tts::align_up((size_t)c->max_alloc * sizeof(tts::CowCopy));
   c->ws_mark = (int32_t*)w;
   w += tts::align_up((size_t)cfg->num_pages * 4);
+  c->ws_items = (int4*)w;
+  w += tts::align_up(rws * cfg->max_pages_per_beam * 16);
+  c->ws_counts = (int32_t*)w;
+  w += tts::align_up(rws * 4);
   c->ws_upload = w;
   if (cudaMallocHost(&c->pinned, (size_t)tts::kUploadSlots * tts::kUploadSlotBytes) != cudaSuccess) {
     delete c;
@@ -294,6 +301,13 @@ static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const ui
       if (d.active) out.push_back(d);
     }
   }
+  // page-list capacity of each group = sum of its active beams' pages
+  int32_t off = 0;
+  for (auto& d : out) {
+    d.pad[0] = off;
+    for (int k = 0; k < d.nbeams; ++k)
+      if ((d.active >> k) & 1u) off += (c->lens[(int64_t)d.req * g.max_beams + d.beam0 + k] + P - 1) / P;
+  }
 }
 
 tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t layer_end,
@@ -324,12 +338,27 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
     plan_groups(c, n_req, req_ids, active, gb, groups);
     if (groups.empty()) return TTS_OK;
     const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
+    // slices per tile: fill the GPU and minimise the idle tail of the last wave
+    // (2 CTAs per SM); a small penalty per extra slice covers the cluster merge
     int splits = 1;
-    if (const char* s = std::getenv("TTS_SPLITS")) splits = std::max(1, std::min(8, std::atoi(s)));
-    else
-      while (splits < 8 && ctas * splits < 2ll * c->num_sms) splits *= 2;
+    if (const char* s = std::getenv("TTS_SPLITS")) {
+      splits = std::max(1, std::min(8, std::atoi(s)));
+    } else {
+      double best = -1.0;
+      for (int sp : {1, 2, 4, 8}) {
+        const double waves = (double)(ctas * sp) / (2.0 * c->num_sms);
+        const double eff = waves / std::ceil(waves) - 0.03 * std::log2((double)sp);
+        if (eff > best + 1e-9) {
+          best = eff;
+          splits = sp;
+        }
+      }
+    }
     void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
     TTS_CUDA(e);
+    int max_np = 0;
+    for (const auto& gd : groups) max_np = std::max(max_np, gd.max_npages);
+    TTS_CUDA(tts::launch_plan(c, (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) prof_pair(c, &e0, &e1);
     if (e0) TTS_CUDA(cudaEventRecord(e0, st));

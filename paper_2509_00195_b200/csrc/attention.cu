@@ -465,6 +465,21 @@ bool make_tensor_maps(Ctx* c) {
                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   c->tmap_ok = (r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS);
+  // 3D view: x = 64 columns (128 B), y = token rows, z = the two 64-column halves
+  cuuint64_t dims3[3] = {64, rows, 2};
+  cuuint64_t strides3[2] = {(cuuint64_t)g.head_dim * 2, 128};
+  cuuint32_t box3[3] = {64, (cuuint32_t)g.page_size, 2};
+  cuuint32_t es3[3] = {1, 1, 1};
+  c->tmap3_ok = false;
+  if (g.head_dim == 128) {
+    CUresult r3 = enc(&c->tmap3_k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c->buf.k_pool, dims3, strides3, box3, es3,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r4 = enc(&c->tmap3_v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c->buf.v_pool, dims3, strides3, box3, es3,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    c->tmap3_ok = (r3 == CUDA_SUCCESS && r4 == CUDA_SUCCESS);
+  }
   return c->tmap_ok;
 }
 

@@ -31,7 +31,7 @@ struct GroupDesc {
   int32_t nbeams;      // beams in the group (<= 32)
   uint32_t active;     // bit i: beam0 + i active
   int32_t max_npages;  // max over active beams of ceil(len / P)
-  int32_t pad[2];
+  int32_t pad[2];  // pad[0]: offset of the group's page list in ws_items
 };
 
 // Allocation item: table entry to receive a fresh page.
@@ -76,6 +76,12 @@ struct Ctx {
   // TMA descriptors (K / V pools, 2D view [rows][d])
   CUtensorMap tmap_k, tmap_v;
   bool tmap_ok = false;
+  // 3D view [2 (d halves)][rows][64] of the same pools: one TMA = one 16x128 tile
+  CUtensorMap tmap3_k, tmap3_v;
+  bool tmap3_ok = false;
+  // attention plan (a3): per-group distinct-page lists
+  int4* ws_items = nullptr;   // [max_requests * max_beams * max_pages_per_beam]
+  int32_t* ws_counts = nullptr;  // [max_requests * max_beams]
 };
 
 // Device-copy a host blob through the pinned ring; returns device pointer.
@@ -107,6 +113,8 @@ bool make_tensor_maps(Ctx* c);
 // attention_umma.cu (tcgen05 path: d = 128, 4 <= G <= 16)
 bool umma_supported(const Ctx* c);
 int umma_max_beams(const Ctx* c);
+cudaError_t launch_plan(Ctx* c, const GroupDesc* groups_d, int n_groups, int max_npages, int max_nbeams,
+                        cudaStream_t s);
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_groups, int splits,
                                   int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
                                   float scale, float* out, cudaStream_t s);
