@@ -38,17 +38,30 @@ constexpr int kNS = 6;                       // ring slots (units)
 constexpr int kTile = kP * kD * 2;           // 4 KiB: one (page, kv head) K or V tile
 constexpr int kSlot = 2 * kU * kTile;        // 16 KiB: K tiles then V tiles
 constexpr int kRing = kNS * kSlot;           // 64 KiB
-constexpr int kThreads = 192;                // warps 0-3 softmax, 4 producer, 5 MMA
+constexpr int kThreads = 256;                // warps 0-3 softmax, 4 producer, 5 MMA, 6-7 V converters
 constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
 constexpr int kSCols = kU * kP;              // 32
 
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 6;        // full, empty, sfull[2], pfull[2], pv[2]
+constexpr int kNumBars = 3 * kNS + 6;        // full, empty, vready, sfull[2], pfull[2], pv[2]
 constexpr int kOffML = kOffBar + kNumBars * 8 + 16;
 constexpr int kSmemBytes = kOffML + 2 * kRows * 4 + 1024;
 static_assert(kRing >= kRows * kD * 4, "merge area must hold a 128x128 fp32 tile");
+
+#ifdef TTS_TRACE
+__device__ long long g_trace[1024][8];
+#define TTS_TR(j, ev)                                                                   \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
+      g_trace[(j)][(ev)] = clock64();                                                   \
+  } while (0)
+#else
+#define TTS_TR(j, ev) \
+  do {                \
+  } while (0)
+#endif
 
 struct UParams {
   const int32_t* lens;
@@ -150,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   float* m_s = reinterpret_cast<float*>(bp + kOffML);
   float* l_s = m_s + kRows;
-  const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
+  const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_vready = b_empty + 8 * kNS,
+                 b_sfull = b_vready + 8 * kNS, b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (*(volatile int32_t*)p.status) return;
@@ -165,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < kNS; ++i) {
       bar_init(b_full + 8 * i, 1);
       bar_init(b_empty + 8 * i, 1);
+      bar_init(b_vready + 8 * i, kU);
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(b_sfull + 8 * i, 1);
@@ -274,12 +288,64 @@ __global__ void __launch_bounds__(kThreads, 2)
       meta[slot * kU] = make_int4(-1, 0, 0, 0);
       bar_arrive(b_full + 8 * slot);
     }
+  } else if (warp >= 6) {
+    // ============================ V converters ============================
+    // Warp 6 + k converts page k of each unit: bf16 -> fp16 in place (exact for
+    // |v| < 2^16; a finite |v| >= 2^16 raises the sticky TTS_ERR_UNSUPPORTED
+    // status) and zeroes token slots >= ntok of a partial page, so that PV is
+    // one fp16 x fp16 MMA per page with fp16 P (SURVEY ledger C14: fp16 P with
+    // V in fp16 stays <= 3.6e-4 row-normwise).
+    const int k = warp - 6;
+    int slot = 0;
+    uint32_t ph = 0;
+    uint32_t vmax = 0;  // running max of |v| as bf16x2 bits (per half)
+    for (int u = u0; u < u1; ++u) {
+      bar_wait(b_full + 8 * slot, ph);
+      const int4 m = meta[slot * kU + k];
+      if (m.x >= 0) {
+        uint4* vt = reinterpret_cast<uint4*>(bp + kOffRing + slot * kSlot + (kU + k) * kTile);
+        if (m.z == kP) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint4 v = vt[i * 32 + lane];
+            vmax = bf16x2_absmax(vmax, v.x, v.y, v.z, v.w);
+            vt[i * 32 + lane] = make_uint4(f16x2_from_bf16x2(v.x), f16x2_from_bf16x2(v.y), f16x2_from_bf16x2(v.z),
+                                           f16x2_from_bf16x2(v.w));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = i * 32 + lane;  // 16-B chunk of the [2][16 tokens][128 B] tile
+            uint4 v = vt[c];
+            if (((c >> 3) & 15) < m.z) {
+              vmax = bf16x2_absmax(vmax, v.x, v.y, v.z, v.w);
+              v = make_uint4(f16x2_from_bf16x2(v.x), f16x2_from_bf16x2(v.y), f16x2_from_bf16x2(v.z),
+                             f16x2_from_bf16x2(v.w));
+            } else {
+              v = make_uint4(0, 0, 0, 0);
+            }
+            vt[c] = v;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(b_vready + 8 * slot);
+      if (++slot == kNS) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+    // finite |v| >= 2^16 (bf16 exponent field 0x8F..0xFE) does not fit fp16
+    const uint32_t e_hi = (vmax >> 23) & 0xFF, e_lo = (vmax >> 7) & 0xFF;
+    const bool big = (e_hi >= 0x8F && e_hi < 0xFF) || (e_lo >= 0x8F && e_lo < 0xFF);
+    if (__any_sync(0xffffffffu, big) && lane == 0) atomicExch(p.status, (int32_t)TTS_ERR_UNSUPPORTED);
   } else if (warp == 5) {
     // ============================ MMA issuer ============================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
     // elected lane issues the tcgen05 instructions.
     constexpr uint32_t id_s = idesc_bf16(kRows, kP, false);
-    constexpr uint32_t id_pv = idesc_bf16(kRows, kD, true);
+    constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
     const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);    // K tiles: K-major SW128
     const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
     auto issue_s = [&](int j) {
@@ -311,7 +377,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t acc = 0;
     for (int j = 0; !done; ++j) {
       const int sn = (j + 1) % kNS;
+      if (lane == 0) TTS_TR(j, 0);
       bar_wait(b_full + 8 * sn, ((j + 1) / kNS) & 1u);
+      if (lane == 0) TTS_TR(j, 1);
       tc_fence_after();
       const bool last = meta[sn * kU].x == -1;
       if (last) {
@@ -321,8 +389,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         issue_s(j + 1);
       }
       bar_wait(b_pfull + 8 * (j & 1), (j >> 1) & 1u);
-      tc_fence_after();
+      if (lane == 0) TTS_TR(j, 2);
       const int slot = j % kNS;
+      bar_wait(b_vready + 8 * slot, (j / kNS) & 1u);  // V converted to fp16
+      tc_fence_after();
       const uint32_t pa = t_s + (j & 1) * kSCols;
       const bool e = elect_one();
 #pragma unroll
@@ -331,13 +401,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
         if (e) {
           mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
-          mma_ts(t_o, pa + kSCols / 2 + k * (kP / 2), dv, id_pv, 1);
         }
         acc = 1;
       }
       if (e) {
         tc_commit(b_empty + 8 * slot);
         tc_commit(b_pv + 8 * (j & 1));
+        TTS_TR(j, 3);
       }
       __syncwarp();
       done = last;
@@ -348,75 +418,89 @@ __global__ void __launch_bounds__(kThreads, 2)
     float m_ref = -1e30f, l = 0.f;
     int j = 0;
     for (;; ++j) {
+      if (r == 0) TTS_TR(j, 4);
       bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
+      if (r == 0) TTS_TR(j, 5);
       tc_fence_after();
       const int slot = j % kNS;
       int4 mt[kU];
 #pragma unroll
       for (int k = 0; k < kU; ++k) mt[k] = meta[slot * kU + k];
       if (mt[0].x == -1) break;
-      uint32_t sr[kSCols];
-      tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
-      tc_wait_ld();
-      float s[kSCols];
-      float mx = -INFINITY;
+      // warp-uniform page membership: a warp none of whose rows reads a page
+      // skips its exponentials (P = 0 there); most private pages touch 1 warp
+      bool mem[kU], wm[kU];
 #pragma unroll
       for (int k = 0; k < kU; ++k) {
-        const bool mem = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
-#pragma unroll
-        for (int c = 0; c < kP; ++c) {
-          const float x = __uint_as_float(sr[k * kP + c]) * p.scale_log2;
-          s[k * kP + c] = (mem && c < mt[k].z) ? x : -INFINITY;
-          mx = fmaxf(mx, s[k * kP + c]);
-        }
+        mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
+        wm[k] = __any_sync(0xffffffffu, mem[k]);
       }
-      const bool need = mx > m_ref + 8.0f;
-      if (__any_sync(0xffffffffu, need) && j > 0) {
-        // every earlier PV product must have landed before O is rescaled in TMEM
-        bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
-        tc_fence_after();
-        const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+      uint32_t ph16[kSCols / 2];
+      if (wm[0] || wm[1]) {
+        uint32_t sr[kSCols];
+        tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
+        tc_wait_ld();
+        // raw scores (scale > 0 commutes with max); masked entries -> -inf
+        float v[kSCols];
+#pragma unroll
+        for (int k = 0; k < kU; ++k)
+#pragma unroll
+          for (int c = 0; c < kP; ++c)
+            v[k * kP + c] = (mem[k] && c < mt[k].z) ? __uint_as_float(sr[k * kP + c]) : -INFINITY;
+        float t[11];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) t[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+        t[10] = fmaxf(v[30], v[31]);
+        t[0] = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmax3(t[6], t[7], fmax3(t[8], t[9], t[10])));
+        const float mx = t[0] * p.scale_log2;
+        const bool need = mx > m_ref + 8.0f;
+        if (__any_sync(0xffffffffu, need) && j > 0) {
+          // every earlier PV product must have landed before O is rescaled in TMEM
+          bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
+          tc_fence_after();
+          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
 #pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t o[32];
-          tc_ld32(t_o + lane_off + ch * 32, o);
-          tc_wait_ld();
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tc_ld32(t_o + lane_off + ch * 32, o);
+            tc_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tc_st32(t_o + lane_off + ch * 32, o);
-        }
-        tc_wait_st();
-        l *= alpha;
-      }
-      if (need) m_ref = mx;
-      uint32_t ph16[kSCols / 2], pl16[kSCols / 2];
-#pragma unroll
-      for (int c = 0; c < kSCols; c += 2) {
-        const float a = ex2(s[c] - m_ref), b = ex2(s[c + 1] - m_ref);
-        l += a + b;
-        const uint32_t h = pack_bf16x2(a, b);
-        ph16[c / 2] = h;
-        pl16[c / 2] = pack_bf16x2(a - bf16lo(h), b - bf16hi(h));
-      }
-      // stale token slots >= ntok of a partial page: zero V so that P (= 0) x V
-      // cannot produce NaN (pool slots past a beam's length are never written)
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        if (mt[k].x >= 0 && mt[k].z < kP) {
-          uint8_t* vt = bp + kOffRing + slot * kSlot + (kU + k) * kTile;
-          for (int idx = r; idx < (kP - mt[k].z) * 16; idx += 128) {
-            const int tok = mt[k].z + idx / 16, ch = idx % 16;
-            *reinterpret_cast<uint4*>(vt + (ch >> 3) * 2048 + tok * 128 + (ch & 7) * 16) = make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tc_st32(t_o + lane_off + ch * 32, o);
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_wait_st();
+          l *= alpha;
         }
+        if (need) m_ref = mx;
+        const float2 nm2 = make_float2(-m_ref, -m_ref);
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        float2 lacc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          if (wm[k]) {
+#pragma unroll
+            for (int c = 0; c < kP; c += 2) {
+              const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
+              const float a = ex2(x.x), b = ex2(x.y);
+              lacc = fadd2(lacc, make_float2(a, b));
+              ph16[(k * kP + c) / 2] = pack_f16x2(a, b);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kP; c += 2) ph16[(k * kP + c) / 2] = 0u;
+          }
+        }
+        l += lacc.x + lacc.y;
+      } else {
+#pragma unroll
+        for (int i = 0; i < kSCols / 2; ++i) ph16[i] = 0u;
       }
-      // P overwrites this unit's S columns: hi at [0,16), lo at [16,32)
+      // P (fp16) overwrites this unit's first 16 S columns: page k at +8k
       tc_st16(t_s + lane_off + (j & 1) * kSCols, ph16);
-      tc_st16(t_s + lane_off + (j & 1) * kSCols + kSCols / 2, pl16);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (r == 0) TTS_TR(j, 6);
       if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
     }
     const int n_done = j;
@@ -531,6 +615,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 }  // namespace
+
+#ifdef TTS_TRACE
+extern "C" int tts_debug_read_trace(long long* out_h) {
+  return (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
+}
+#endif
 
 bool umma_supported(const Ctx* c) {
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
