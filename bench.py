@@ -188,33 +188,49 @@ class Bench:
             self._chk(lib.tts_block_table_init_request(h, self.local[r], c.N, c.prompt, k.data_ptr(),
                                                        v.data_ptr(), st), "init")
         nr = len(self.ring)
+        ptrs = [(ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()), ctypes.c_void_p(v.data_ptr()))
+                for q, k, v in self.ring]
+        outp = ctypes.c_void_p(self.out.data_ptr())
+        decode = lib.tts_decode_step
         for it in self.sched:
             q, k, v = self.ring[it.t % nr]
-            if e2e is not None:
-                hq, hk, hv = e2e["ring"][it.t % nr]
-                q = e2e["q"]
-                k = e2e["k"]
-                v = e2e["v"]
-                q.copy_(hq, non_blocking=True)
-                k.copy_(hk, non_blocking=True)
-                v.copy_(hv, non_blocking=True)
-            if self.batched:
-                loc = [self.local[r] for r in it.reqs]
-                arr = (ctypes.c_int32 * len(loc))(*loc)
-                act = np.ascontiguousarray(np.stack(it.active), dtype=np.uint8)
-                self._chk(lib.tts_decode_step(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
-                                              k.data_ptr(), v.data_ptr(), q.data_ptr(), self.scale,
-                                              self.out.data_ptr(), st), "decode_step")
-                if stats_accum is not None:
-                    self._chk(lib.tts_block_table_stats(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
-                                                        stats_accum.data_ptr(), st), "stats")
-            else:
+            if e2e is None and not self.batched and stats_accum is None:
+                # hot loop: one C-ABI call per request and position, arguments pre-marshalled
+                qp, kp, vp = ptrs[it.t % nr]
                 for r in it.reqs:
-                    arr = self.req_arr[self.local[r]]
-                    self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
-                                                  self.scale, self.out.data_ptr(), st), "decode_step")
+                    rc = decode(h, 1, self.req_arr[self.local[r]], None, kp, vp, qp, self.scale, outp, st)
+                    if rc:
+                        self._chk(rc, "decode_step")
+            else:
+                if e2e is not None:
+                    hq, hk, hv = e2e["ring"][it.t % nr]
+                    q = e2e["q"]
+                    k = e2e["k"]
+                    v = e2e["v"]
+                    q.copy_(hq, non_blocking=True)
+                    k.copy_(hk, non_blocking=True)
+                    v.copy_(hv, non_blocking=True)
+                if self.batched:
+                    loc = [self.local[r] for r in it.reqs]
+                    arr = (ctypes.c_int32 * len(loc))(*loc)
+                    act = np.ascontiguousarray(np.stack(it.active), dtype=np.uint8)
+                    self._chk(lib.tts_decode_step(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
+                                                  k.data_ptr(), v.data_ptr(), q.data_ptr(), self.scale,
+                                                  self.out.data_ptr(), st), "decode_step")
                     if stats_accum is not None:
-                        self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum.data_ptr(), st), "stats")
+                        self._chk(lib.tts_block_table_stats(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
+                                                            stats_accum.data_ptr(), st), "stats")
+                else:
+                    for ri, r in enumerate(it.reqs):
+                        if e2e is not None and ri > 0:  # every call's q/k/v come from the host
+                            q.copy_(hq, non_blocking=True)
+                            k.copy_(hk, non_blocking=True)
+                            v.copy_(hv, non_blocking=True)
+                        arr = self.req_arr[self.local[r]]
+                        self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
+                                                      self.scale, self.out.data_ptr(), st), "decode_step")
+                        if stats_accum is not None:
+                            self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum.data_ptr(), st), "stats")
             if it.forks:
                 loc = [self.local[r] for r, _ in it.forks]
                 arr = (ctypes.c_int32 * len(loc))(*loc)
@@ -344,8 +360,10 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(st)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         b.run_step()
+    host_s = time.perf_counter() - h0  # host enqueue time (the GPU may still be running)
     e1.record(st)
     torch.cuda.synchronize(dev)
     barrier(ws)
@@ -423,6 +441,7 @@ def main():
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "host_enqueue_ms_per_step": host_s * 1e3 / args.steps,
             "clocks": clk,
         }
         print(json.dumps(line))

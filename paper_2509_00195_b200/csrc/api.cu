@@ -2,7 +2,6 @@
 // mirror of beam lengths, launch planning, workspace carving.  Every step of
 // the hot path runs in the kernels of block_table.cu / attention.cu.
 #include <algorithm>
-#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -47,6 +46,30 @@ void* upload(Ctx* c, const void* src, size_t bytes, cudaStream_t st, cudaError_t
   *err = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st);
   if (*err == cudaSuccess) *err = cudaEventRecord(c->ev[slot], st);
   return d;
+}
+
+// Two blobs through one pinned slot and one copy (the per-call descriptors of
+// the hot path: group list + append slots).
+void upload2(Ctx* c, const void* a, size_t na, const void* b, size_t nb, cudaStream_t st, cudaError_t* err,
+             void** da, void** db) {
+  *err = cudaSuccess;
+  const size_t off = (na + 255) / 256 * 256;
+  if (off + nb > kUploadSlotBytes) {
+    *da = upload(c, a, na, st, err);
+    if (*err == cudaSuccess) *db = upload(c, b, nb, st, err);
+    return;
+  }
+  const int slot = c->up_pos;
+  c->up_pos = (c->up_pos + 1) % kUploadSlots;
+  cudaEventSynchronize(c->ev[slot]);
+  uint8_t* h = c->pinned + (size_t)slot * kUploadSlotBytes;
+  uint8_t* d = c->ws_upload + (size_t)slot * kUploadSlotBytes;
+  std::memcpy(h, a, na);
+  std::memcpy(h + off, b, nb);
+  *err = cudaMemcpyAsync(d, h, off + nb, cudaMemcpyHostToDevice, st);
+  if (*err == cudaSuccess) *err = cudaEventRecord(c->ev[slot], st);
+  *da = d;
+  *db = d + off;
 }
 
 }  // namespace tts
@@ -231,9 +254,13 @@ tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_be
   return TTS_OK;
 }
 
+// Validates, allocates the pages beams crossing a page boundary need (device
+// allocator) and advances the host length mirror.  The K/V write is launched
+// here unless `deferred` is given, in which case the slot list is returned for
+// the fused append + plan kernel of tts_decode_step.
 static tts_status_t append_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
                                 const uint8_t* active, const void* k_new, const void* v_new,
-                                void* stream) {
+                                void* stream, std::vector<int32_t>* deferred = nullptr) {
   if (!c || n_req <= 0 || !req_ids || !k_new || !v_new) return TTS_ERR_INVALID_ARG;
   const tts_config_t& g = c->cfg;
   const int P = g.page_size;
@@ -257,13 +284,14 @@ static tts_status_t append_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_i
     TTS_CUDA(e);
     TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
   }
-  if (!slots.empty()) {
+  if (!slots.empty() && !deferred) {
     void* d = tts::upload(c, slots.data(), slots.size() * 4, st, &e);
     TTS_CUDA(e);
     TTS_CUDA(tts::launch_append_write(c, (const int32_t*)d, (int)slots.size() / 4, n_req,
                                       (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
   }
   for (size_t k = 0; k < slots.size(); k += 4) c->lens[(int64_t)slots[k + 1] * g.max_beams + slots[k + 2]]++;
+  if (deferred) deferred->swap(slots);
   return TTS_OK;
 }
 
@@ -310,9 +338,13 @@ static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const ui
   }
 }
 
-tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t layer_end,
-                                    int32_t n_req, const int32_t* req_ids, const uint8_t* active,
-                                    const void* q, float scale, float* out, void* stream) {
+// Attention for the call; `pending` (tts_decode_step) carries append slots whose
+// K/V write has not been launched yet: fused with the plan on the tcgen05 path,
+// launched just before the attention kernel otherwise.
+static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_end, int32_t n_req,
+                              const int32_t* req_ids, const uint8_t* active, const void* q, float scale,
+                              float* out, void* stream, const std::vector<int32_t>* pending = nullptr,
+                              const void* k_new = nullptr, const void* v_new = nullptr) {
   if (!c || !req_ids || !q || !out || n_req <= 0) return TTS_ERR_INVALID_ARG;
   const tts_config_t& g = c->cfg;
   if (layer_begin < 0 || layer_end > g.num_layers || layer_begin >= layer_end) return TTS_ERR_INVALID_ARG;
@@ -338,27 +370,31 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
     plan_groups(c, n_req, req_ids, active, gb, groups);
     if (groups.empty()) return TTS_OK;
     const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
-    // slices per tile: fill the GPU and minimise the idle tail of the last wave
-    // (2 CTAs per SM); a small penalty per extra slice covers the cluster merge
+    // slices per tile (a cluster): the smallest split that puts >= 3/4 of a wave
+    // (2 CTAs per SM) on the GPU; measured on C2 / C3 shapes, longer CTAs beat
+    // extra waves because each CTA's unit pipeline has a fixed ramp
     int splits = 1;
     if (const char* s = std::getenv("TTS_SPLITS")) {
       splits = std::max(1, std::min(8, std::atoi(s)));
     } else {
-      double best = -1.0;
-      for (int sp : {1, 2, 4, 8}) {
-        const double waves = (double)(ctas * sp) / (2.0 * c->num_sms);
-        const double eff = waves / std::ceil(waves) - 0.03 * std::log2((double)sp);
-        if (eff > best + 1e-9) {
-          best = eff;
-          splits = sp;
-        }
-      }
+      while (splits < 8 && ctas * splits * 4 < 3ll * 2 * c->num_sms) splits *= 2;
     }
-    void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
-    TTS_CUDA(e);
     int max_np = 0;
     for (const auto& gd : groups) max_np = std::max(max_np, gd.max_npages);
-    TTS_CUDA(tts::launch_plan(c, (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
+    void* d = nullptr;
+    void* ds = nullptr;
+    if (pending && !pending->empty()) {
+      tts::upload2(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), pending->data(), pending->size() * 4,
+                   st, &e, &d, &ds);
+      TTS_CUDA(e);
+      TTS_CUDA(tts::launch_append_plan(c, (const int32_t*)ds, (int)pending->size() / 4, n_req,
+                                       (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
+                                       (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
+    } else {
+      d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
+      TTS_CUDA(e);
+      TTS_CUDA(tts::launch_plan(c, (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) prof_pair(c, &e0, &e1);
     if (e0) TTS_CUDA(cudaEventRecord(e0, st));
@@ -380,6 +416,12 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
     if (forced || ctas >= 2ll * c->num_sms) break;
   }
   if (!chosen) return TTS_ERR_UNSUPPORTED;
+  if (pending && !pending->empty()) {
+    void* ds = tts::upload(c, pending->data(), pending->size() * 4, st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_append_write(c, (const int32_t*)ds, (int)pending->size() / 4, n_req,
+                                      (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
+  }
   if (groups.empty()) return TTS_OK;
   void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
   TTS_CUDA(e);
@@ -392,12 +434,21 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t la
   return TTS_OK;
 }
 
+tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t layer_end,
+                                    int32_t n_req, const int32_t* req_ids, const uint8_t* active,
+                                    const void* q, float scale, float* out, void* stream) {
+  return attn_impl(c, layer_begin, layer_end, n_req, req_ids, active, q, scale, out, stream);
+}
+
 tts_status_t tts_decode_step(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
                              const uint8_t* active, const void* k_new, const void* v_new,
                              const void* q, float scale, float* out, void* stream) {
-  tts_status_t s = append_impl(c, n_req, req_ids, active, k_new, v_new, stream);
+  if (!c || !q || !out) return TTS_ERR_INVALID_ARG;
+  std::vector<int32_t> pending;
+  tts_status_t s = append_impl(c, n_req, req_ids, active, k_new, v_new, stream, &pending);
   if (s != TTS_OK) return s;
-  return tts_prefix_attn_decode(c, 0, c->cfg.num_layers, n_req, req_ids, active, q, scale, out, stream);
+  return attn_impl(c, 0, c->cfg.num_layers, n_req, req_ids, active, q, scale, out, stream, &pending, k_new,
+                   v_new);
 }
 
 static constexpr int kProfPairs = 4096;

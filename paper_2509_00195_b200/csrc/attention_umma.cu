@@ -77,28 +77,36 @@ struct UParams {
 };
 
 // ---------------------------------------------------------------------------
-// a3: plan.  One CTA per group, one warp per position (32 positions a round).
-__global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ tables, const int32_t* __restrict__ lens,
-                                              const GroupDesc* __restrict__ groups, int4* __restrict__ items,
-                                              int32_t* __restrict__ counts, const int32_t* status, int maxB,
-                                              int maxP) {
-  extern __shared__ int32_t tb[];  // [nbeams][npg + 1]
+// a3: plan.  One CTA per group, one warp per position (NT/32 positions a round).
+template <int NT>
+__device__ __forceinline__ void plan_group(const GroupDesc& g, int gi, const int32_t* __restrict__ tables,
+                                           int32_t* __restrict__ lens, int4* __restrict__ items,
+                                           int32_t* __restrict__ counts, int maxB, int maxP, int32_t* tb,
+                                           bool bump) {
+  constexpr int NW = NT / 32;
   __shared__ int s_len[32];
   __shared__ int s_cnt[32];
   __shared__ int s_off[32];
   __shared__ int s_tot;
-  if (*(volatile const int32_t*)status) return;
-  const GroupDesc g = groups[blockIdx.x];
   const int nb = g.nbeams, npg = g.max_npages, ld = npg + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < 32) s_len[tid] = (tid < nb && ((g.active >> tid) & 1u)) ? lens[(int64_t)g.req * maxB + g.beam0 + tid] : 0;
+  if (tid < 32) {
+    const bool act = tid < nb && ((g.active >> tid) & 1u);
+    int len = act ? lens[(int64_t)g.req * maxB + g.beam0 + tid] : 0;
+    if (act && bump) {  // fused with the append: the active beams' new token
+      len += 1;
+      lens[(int64_t)g.req * maxB + g.beam0 + tid] = len;
+    }
+    s_len[tid] = len;
+  }
   __syncthreads();
+  // the group's table rows -> smem, all loads in flight before any store
   const int n = nb * npg;
-  for (int b0 = tid; b0 < n; b0 += 8 * 1024) {
+  for (int b0 = tid; b0 < n; b0 += 8 * NT) {
     int v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int idx = b0 + k * 1024;
+      const int idx = b0 + k * NT;
       v[k] = -1;
       if (idx < n) {
         const int b = idx / npg, i = idx % npg;
@@ -107,15 +115,16 @@ __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ table
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int idx = b0 + k * 1024;
+      const int idx = b0 + k * NT;
       if (idx < n) tb[(idx / npg) * ld + idx % npg] = v[k];
     }
   }
   __syncthreads();
   int4* out = items + g.pad[0];
   int base = 0;
-  for (int i0 = 0; i0 < npg; i0 += 32) {
+  for (int i0 = 0; i0 < npg; i0 += NW) {
     const int i = i0 + warp;
+    // runs of equal page ids over adjacent beams (DFS order: sharers are adjacent)
     const bool has = i < npg && lane < nb && tb[lane * ld + i] >= 0;
     const int page = has ? tb[lane * ld + i] : -1;
     const uint32_t hm = __ballot_sync(0xffffffffu, has);
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ table
     if (lane == 0) s_cnt[warp] = __popc(sm);
     __syncthreads();
     if (warp == 0) {
-      const int c = s_cnt[lane];
+      const int c = lane < NW ? s_cnt[lane] : 0;
       int x = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -148,7 +157,77 @@ __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ table
     base += s_tot;
     __syncthreads();
   }
-  if (tid == 0) counts[blockIdx.x] = base;
+  if (tid == 0) counts[gi] = base;
+}
+
+__global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ tables, int32_t* __restrict__ lens,
+                                              const GroupDesc* __restrict__ groups, int4* __restrict__ items,
+                                              int32_t* __restrict__ counts, const int32_t* status, int maxB,
+                                              int maxP) {
+  extern __shared__ int32_t tb[];  // [nbeams][npg + 1]
+  if (*(volatile const int32_t*)status) return;
+  plan_group<1024>(groups[blockIdx.x], blockIdx.x, tables, lens, items, counts, maxB, maxP, tb, false);
+}
+
+// a2 + a3 fused (tts_decode_step): blocks [0, n_slots) append one token of one
+// beam for every layer (slot item = call, req, beam, pos), blocks [n_slots,
+// n_slots + n_groups) build the attention plan and advance the lengths of the
+// group's active beams (each beam belongs to exactly one group).  The plan
+// reads only block tables (pages were allocated before this launch) and the
+// pre-append lengths, so the two roles are independent.
+struct AppendPlanParams {
+  __nv_bfloat16* k_pool;
+  __nv_bfloat16* v_pool;
+  const int32_t* tables;
+  int32_t* lens;
+  const int4* slots;
+  int n_slots, n_call;
+  const uint4* k_new;
+  const uint4* v_new;
+  const GroupDesc* groups;
+  int4* items;
+  int32_t* counts;
+  const int32_t* status;
+  int L, Hkv, d, maxB, maxP;
+  int64_t num_pages;
+};
+
+__global__ void __launch_bounds__(256) k_append_plan(AppendPlanParams p) {
+  extern __shared__ int32_t tb[];
+  if (*(volatile const int32_t*)p.status) return;
+  if ((int)blockIdx.x >= p.n_slots) {
+    const int gi = blockIdx.x - p.n_slots;
+    plan_group<256>(p.groups[gi], gi, p.tables, p.lens, p.items, p.counts, p.maxB, p.maxP, tb, true);
+    return;
+  }
+  const int4 it = p.slots[blockIdx.x];
+  const int call = it.x, req = it.y, beam = it.z, pos = it.w;
+  const int vpr = p.d / 8;  // 16-B vectors per (token, kv head) row
+  const int n = p.Hkv * vpr, total = p.L * n;
+  const int32_t page = p.tables[((int64_t)req * p.maxB + beam) * p.maxP + pos / kP];
+  // all layers at once: 4 independent 16-B copies in flight per thread
+  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * (int)blockDim.x) {
+    uint4 kv[4], vv[4];
+    int64_t dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < total) {
+        const int l = i / n, r2 = i % n, kh = r2 / vpr, e = r2 % vpr;
+        const int64_t src = ((((int64_t)l * p.n_call + call) * p.maxB + beam) * p.Hkv + kh) * vpr + e;
+        dst[u] = ((((int64_t)l * p.num_pages + page) * p.Hkv + kh) * kP + pos % kP) * vpr + e;
+        kv[u] = p.k_new[src];
+        vv[u] = p.v_new[src];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u * (int)blockDim.x < total) {
+        reinterpret_cast<uint4*>(p.k_pool)[dst[u]] = kv[u];
+        reinterpret_cast<uint4*>(p.v_pool)[dst[u]] = vv[u];
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -644,6 +723,42 @@ cudaError_t launch_plan(Ctx* c, const GroupDesc* groups_d, int n_groups, int max
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   k_plan<<<n_groups, 1024, smem, st>>>(c->buf.block_tables, c->buf.seq_lens, groups_d, c->ws_items, c->ws_counts,
                                        c->buf.status, c->cfg.max_beams, c->cfg.max_pages_per_beam);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_append_plan(Ctx* c, const int32_t* slots_d, int n_slots, int n_call, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, const GroupDesc* groups_d, int n_groups, int max_npages,
+                               int max_nbeams, cudaStream_t st) {
+  const int smem = max_nbeams * (max_npages + 1) * 4;
+  static int smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_append_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    smem_set = 200 * 1024;
+  }
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  AppendPlanParams p;
+  p.k_pool = (__nv_bfloat16*)c->buf.k_pool;
+  p.v_pool = (__nv_bfloat16*)c->buf.v_pool;
+  p.tables = c->buf.block_tables;
+  p.lens = c->buf.seq_lens;
+  p.slots = (const int4*)slots_d;
+  p.n_slots = n_slots;
+  p.n_call = n_call;
+  p.k_new = (const uint4*)k;
+  p.v_new = (const uint4*)v;
+  p.groups = groups_d;
+  p.items = c->ws_items;
+  p.counts = c->ws_counts;
+  p.status = c->buf.status;
+  p.L = c->cfg.num_layers;
+  p.Hkv = c->cfg.num_kv_heads;
+  p.d = c->cfg.head_dim;
+  p.maxB = c->cfg.max_beams;
+  p.maxP = c->cfg.max_pages_per_beam;
+  p.num_pages = c->cfg.num_pages;
+  k_append_plan<<<n_slots + n_groups, 256, smem, st>>>(p);
   c->launches++;
   return cudaGetLastError();
 }

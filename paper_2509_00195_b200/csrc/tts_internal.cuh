@@ -86,6 +86,8 @@ struct Ctx {
 
 // Device-copy a host blob through the pinned ring; returns device pointer.
 void* upload(Ctx* c, const void* src, size_t bytes, cudaStream_t s, cudaError_t* err);
+void upload2(Ctx* c, const void* a, size_t na, const void* b, size_t nb, cudaStream_t s, cudaError_t* err,
+             void** da, void** db);
 
 size_t workspace_bytes(const tts_config_t& cfg);
 
@@ -115,6 +117,9 @@ bool umma_supported(const Ctx* c);
 int umma_max_beams(const Ctx* c);
 cudaError_t launch_plan(Ctx* c, const GroupDesc* groups_d, int n_groups, int max_npages, int max_nbeams,
                         cudaStream_t s);
+cudaError_t launch_append_plan(Ctx* c, const int32_t* slots_d, int n_slots, int n_call, const __nv_bfloat16* k,
+                               const __nv_bfloat16* v, const GroupDesc* groups_d, int n_groups, int max_npages,
+                               int max_nbeams, cudaStream_t s);
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_groups, int splits,
                                   int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
                                   float scale, float* out, cudaStream_t s);

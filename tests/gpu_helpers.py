@@ -36,14 +36,14 @@ def compare_state(snap: dict, tables: List[List[int]], lens: List[int], P: int,
 
 def run_parity(cfg: workload.Config, sample: Callable, num_pages: Optional[int] = None,
                scores_fn: Optional[Callable] = None, max_iters: Optional[int] = None,
-               check_refs: bool = True) -> Dict[str, float]:
+               check_refs: bool = True, fused: bool = True) -> Dict[str, float]:
     from paper_2509_00195_b200.runner import BeamStepRunner
 
     num_pages = num_pages or default_num_pages(cfg, cfg.R)
     orc = OracleRun(cfg, num_pages=num_pages, track_content=cfg.R * cfg.N <= 64)
     tr = orc.run(sample=sample, snapshot_refs=check_refs, scores_fn=scores_fn, max_iters=max_iters)
 
-    runner = BeamStepRunner(cfg, num_pages=num_pages)
+    runner = BeamStepRunner(cfg, num_pages=num_pages, fused=fused)
     ctx = runner.ctx
     # poison the pools: slots that are never written must never reach an output
     ctx.k_pool.fill_(float("nan"))

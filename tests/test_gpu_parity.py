@@ -81,6 +81,17 @@ def _sample_points(cfg, beams, layers, per_step=3):
     return f
 
 
+@pytest.mark.parametrize("path", ["umma", "mma"])
+def test_separate_calls_and_both_kernels(path, monkeypatch):
+    # tts_block_table_append + tts_prefix_attn_decode as two calls (no fusion), on
+    # the tcgen05 path and on the mma.sync path (TTS_ATTN=mma), G = 7, d = 128
+    monkeypatch.setenv("TTS_ATTN", path)
+    cfg = workload.Config("sep", R=2, N=16, M=4, L=2, Hq=14, Hkv=2, d=128, P=16, prompt=37, n_steps=3,
+                          step_len=0, ln_mu=math.log(20), ln_sigma=1.0, ln_cap=60, seed=4242)
+    run_parity(cfg, all_beams(cfg, every=5), fused=False)
+    run_parity(cfg, all_beams(cfg, every=5), fused=True)
+
+
 def test_c2_full_size():
     cfg = workload.C2
     res = run_parity(cfg, _sample_points(cfg, [0, 5, 15], [0, 13, 27]))
