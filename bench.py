@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dump-call-bytes", default="")
     return ap.parse_args()
 
 
@@ -172,6 +173,8 @@ class Bench:
         self.parent = torch.empty(self.n, cfg.N, dtype=torch.int32, device=self.dev)
         self.beam_steps = sum(int(a.sum()) for it in self.sched for a in it.active)
         self.stream = self.ctx.stream
+        self.ncall = 0
+        self.n_calls = sum(1 if self.batched else len(it.reqs) for it in self.sched)
         torch.cuda.synchronize(self.dev)
 
     def _chk(self, code, what):
@@ -219,7 +222,8 @@ class Bench:
                                                   self.out.data_ptr(), st), "decode_step")
                     if stats_accum is not None:
                         self._chk(lib.tts_block_table_stats(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
-                                                            stats_accum.data_ptr(), st), "stats")
+                                                            stats_accum[self.ncall].data_ptr(), st), "stats")
+                        self.ncall += 1
                 else:
                     for ri, r in enumerate(it.reqs):
                         if e2e is not None and ri > 0:  # every call's q/k/v come from the host
@@ -230,7 +234,9 @@ class Bench:
                         self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
                                                       self.scale, self.out.data_ptr(), st), "decode_step")
                         if stats_accum is not None:
-                            self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum.data_ptr(), st), "stats")
+                            self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum[self.ncall].data_ptr(),
+                                                                st), "stats")
+                            self.ncall += 1
             if it.forks:
                 loc = [self.local[r] for r, _ in it.forks]
                 arr = (ctypes.c_int32 * len(loc))(*loc)
@@ -341,13 +347,21 @@ def main():
     st = torch.cuda.current_stream(dev)
 
     # warm-up (the first one also accumulates the unique / logical KV statistics)
-    accum = torch.zeros(2, dtype=torch.int64, device=dev)
+    per_call = torch.zeros(b.n_calls, 2, dtype=torch.int64, device=dev)  # unique / logical tokens per call
     for i in range(max(args.warmup, 1)):
-        b.run_step(stats_accum=accum if i == 0 else None)
+        b.run_step(stats_accum=per_call if i == 0 else None)
     torch.cuda.synchronize(dev)
     assert b.ctx.tts_device_status() == 0, "device status error during warm-up"
-    unique_tok, logical_tok = [int(x) for x in accum.tolist()]
+    unique_tok, logical_tok = [int(x) for x in per_call.sum(0).tolist()]
     kv_tok = 4 * cfg.Hkv * cfg.d * cfg.L  # bytes per token over all layers (bf16 K+V)
+    if args.dump_call_bytes:
+        # algorithmic bytes of every attention launch of one step (to line up with ncu launch ids)
+        active_rows = [int(a.sum()) for it in b.sched for a in (it.active if not b.batched else [np.stack(it.active)])]
+        calls = per_call[:, 0].tolist()
+        json.dump({"config": cfg.name, "kv_bytes_per_token": kv_tok,
+                   "qo_bytes_per_beam": cfg.L * cfg.Hq * cfg.d * 6,
+                   "unique_kv_bytes": [u * kv_tok for u in calls], "active_beams": active_rows},
+                  open(args.dump_call_bytes, "w"))
     unique_b, logical_b = unique_tok * kv_tok, logical_tok * kv_tok
     qo_b = b.beam_steps * cfg.L * cfg.Hq * cfg.d * (2 + 4)
 
@@ -406,11 +420,17 @@ def main():
         e2e = {"value": allsum(b.beam_steps * args.e2e_steps, ws, dev) / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(ctx_e["d2h"])}
 
-    traffic = None
+    # DRAM traffic of one ncu --set full capture of this kernel on this workload
+    # (profiles/ncu_traffic_<cfg>.json, written by tools/profile_summary.py),
+    # scaled to this run's average launch by the captured launch's traffic /
+    # algorithmic-bytes ratio (1.0 = every unique page read from HBM exactly once)
+    traffic, traffic_ratio = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic_ratio = pj["dram_bytes_per_launch"] / pj["algo_bytes_of_that_launch"]
+            traffic = traffic_ratio * (unique_b + qo_b) / max(1, b.n_calls)
         except Exception:
             traffic = None
 
@@ -431,8 +451,9 @@ def main():
                               else "batched requests (working set >> L2)"),
                        "parallelism": f"dp{ws} (independent requests per rank, no data-path collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk, "unit": "GB/s",
-                         "frac": achieved_gbs / pk, "traffic": traffic, "peak_source": pk_src,
-                         "kernel": "k_tree_attn (prefix-shared decode attention)",
+                         "frac": achieved_gbs / pk, "traffic": traffic, "traffic_over_algo": traffic_ratio,
+                         "peak_source": pk_src,
+                         "kernel": "k_tree_umma (tcgen05 prefix-shared decode attention)",
                          "algo_bytes": "unique KV (valid tokens of distinct pages) + q bf16 + out fp32",
                          "unique_kv_gbs": unique_gbs, "logical_kv_gbs": logical_gbs,
                          "reuse": logical_tok / max(unique_tok, 1),
