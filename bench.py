@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dump-call-bytes", default="")
+    ap.add_argument("--requests", type=int, default=0, help="override R of the straggler batch (C4)")
+    ap.add_argument("--pages-per-request", type=int, default=0,
+                    help="page-pool budget per request (default: exact bound for fixed steps, 6000 for C4)")
     return ap.parse_args()
 
 
@@ -140,7 +143,7 @@ class Clocks:
 class Bench:
     """Drives one rank's requests through libtts with minimal host overhead."""
 
-    def __init__(self, cfg, greqs, dev_index, ring=8):
+    def __init__(self, cfg, greqs, dev_index, ring=8, pages_per_request=0):
         from paper_2509_00195_b200 import build
         build.build()
         from paper_2509_00195_b200.runner import tts_config, Inputs
@@ -148,7 +151,7 @@ class Bench:
         self.cfg = cfg
         self.greqs = list(greqs)
         self.n = len(self.greqs)
-        self.tcfg = tts_config(cfg, self.n)
+        self.tcfg = tts_config(cfg, self.n, num_pages=(pages_per_request * self.n + 64) if pages_per_request else None)
         self.ctx = Context(self.tcfg, dev_index)
         self.lib = self.ctx.lib
         self.h = self.ctx.h
@@ -335,15 +338,19 @@ def main():
     dev = torch.device("cuda", local)
     cfg = workload.CONFIGS[args.config]
     rot = args.rotate or DEFAULT_ROTATE[args.config]
+    ppr = args.pages_per_request
     if cfg.step_len == 0:
         # straggler batch: shard the R requests over ranks (request r -> rank r mod G)
+        if args.requests:
+            cfg = cfg.with_(R=args.requests)
         greqs = [r for r in range(cfg.R) if r % ws == rank]
         scaling = "strong"
+        ppr = ppr or 6000  # ~3x the simulated mean live pages of a C4 request
     else:
         cfg = cfg.with_(R=rot * ws)  # independent requests of the same shape, rot per rank
         greqs = [rank * rot + i for i in range(rot)]
         scaling = "weak"
-    b = Bench(cfg, greqs, local)
+    b = Bench(cfg, greqs, local, pages_per_request=ppr)
     st = torch.cuda.current_stream(dev)
 
     # warm-up (the first one also accumulates the unique / logical KV statistics)

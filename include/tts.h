@@ -24,13 +24,14 @@
  *                                 P:181; ledger C3-C8)
  *   tts_block_table_release_request / _snapshot / _stats  lifecycle, debug
  *                                 checkpoint, unique/logical KV accounting
- *   tts_comm_init / tts_beam_select_fork_global  multi-GPU global top-K over
- *                                 NCCL all-gather
+ *   tts_beam_select_global / tts_beam_fork_map / tts_lineage_*  multi-GPU
+ *                                 global top-K over an NCCL all-gather of the
+ *                                 scores, with lineage migration
  *
  * Memory ownership: the CALLER allocates every device buffer described by
  * tts_buffers_t (sizes from tts_query_buffer_bytes) and keeps it alive and
  * unmodified for the lifetime of the context.  libtts owns only its host-side
- * context (and an NCCL communicator if tts_comm_init was called).  Buffers
+ * context.  Buffers
  * passed to individual calls (q, k/v, scores, out) are borrowed until the
  * stream work of that call completes.
  *
@@ -181,6 +182,53 @@ tts_status_t tts_profile_end(tts_ctx_t ctx, double* attn_ms_h, int64_t* attn_lau
 tts_status_t tts_beam_select_fork(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
                                   const float* scores, int32_t width_m, int32_t* parent_out,
                                   void* stream);
+
+/* ---- a8: one request's beams spanning G GPUs --------------
+ * The request's N_global beams are held in G contiguous ranges of global ids
+ * (gid = rank * N_local + local index; DFS order across ranks).  Per step:
+ *   1. the caller all-gathers the N_local scores of every rank (NCCL over
+ *      NVLink via torch.distributed; 4 B per beam) into scores_all;
+ *   2. tts_beam_select_global on every rank computes the same global parent
+ *      map (the single-GPU key, ledger C3/C4, with the global id as index;
+ *      ledger C19), so survivors are identical on every rank;
+ *   3. child gid c is placed on rank c / N_local (children of one survivor are
+ *      consecutive, so each rank's beams stay a DFS-ordered run); a child whose
+ *      parent lives on another rank receives the parent's lineage: the owner
+ *      exports it (tts_lineage_export), the caller ships the buffer
+ *      (NCCL send/recv), the destination imports it into a spare row
+ *      (tts_lineage_import; fresh pages, lowest free ids);
+ *   4. tts_beam_fork_map forks the local rows by an explicit parent map.
+ * Page ids are per rank; survivors, parent maps and every beam's token
+ * sequence equal the single-GPU run (ledger C20). */
+
+/* Global selection over scores_all (device fp32 [n_global], n_global <= 1024,
+ * n_global % width_m == 0).  parent_gid_out: device int32 [n_global],
+ * new gid -> old gid.  No sync. */
+tts_status_t tts_beam_select_global(tts_ctx_t ctx, int32_t n_global, const float* scores_all,
+                                    int32_t width_m, int32_t* parent_gid_out, void* stream);
+
+/* Fork request `req` by an explicit map: new row c (0 <= c < n_new) copies old
+ * row parent_h[c] (host int32 [n_new]; old rows = the request's beams plus
+ * imported lineages).  Refcounts recounted, released pages freed before any
+ * allocation; the first child of each parent keeps a partially filled last
+ * page, later children get a copy (ledger C6-C8).  Syncs. */
+tts_status_t tts_beam_fork_map(tts_ctx_t ctx, int32_t req, int32_t n_new, const int32_t* parent_h,
+                               void* stream);
+
+/* Size of a lineage buffer for a beam of `len` tokens:
+ * bf16 [2 (K, V)][L][len][Hkv][d]. */
+tts_status_t tts_lineage_bytes(tts_ctx_t ctx, int32_t len, size_t* bytes_h);
+
+/* Copy beam `beam` of request `req` (all its tokens, every layer) into buf
+ * (device, tts_lineage_bytes(len) bytes). */
+tts_status_t tts_lineage_export(tts_ctx_t ctx, int32_t req, int32_t beam, void* buf, void* stream);
+
+/* Install a lineage of `len` tokens from buf into the empty row `beam`
+ * (beam >= the request's beam count): allocates ceil(len/P) fresh pages
+ * (lowest free ids) and writes them.  Errors: TTS_ERR_STATE if the row is in
+ * use; pool exhaustion is the sticky device error. */
+tts_status_t tts_lineage_import(tts_ctx_t ctx, int32_t req, int32_t beam, int32_t len, const void* buf,
+                                void* stream);
 
 /* Release every page of request `req` (refcount decrement, free at 0). */
 tts_status_t tts_block_table_release_request(tts_ctx_t ctx, int32_t req, void* stream);

@@ -138,6 +138,7 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   c->n_beams.assign(cfg->max_requests, 0);
+  c->n_rows.assign(cfg->max_requests, 0);
   c->lens.assign((size_t)cfg->max_requests * cfg->max_beams, 0);
   // carve workspace
   uint8_t* w = (uint8_t*)bufs->workspace;
@@ -250,6 +251,7 @@ tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_be
   TTS_CUDA(cudaMemcpyAsync(c->buf.seq_lens + (int64_t)req * g.max_beams, d, lens.size() * 4,
                            cudaMemcpyDeviceToDevice, st));
   c->n_beams[req] = n_beams;
+  c->n_rows[req] = n_beams;
   std::copy(lens.begin(), lens.end(), c->lens.begin() + (int64_t)req * g.max_beams);
   return TTS_OK;
 }
@@ -515,7 +517,9 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   void* dreq = tts::upload(c, req_ids, (size_t)n_req * 4, st, &e);
   TTS_CUDA(e);
   TTS_CUDA(tts::launch_select(c, (const int32_t*)dreq, n_req, scores, N, M, parent_out, st));
-  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, n_req, N, st));
+  for (int i = 0; i < n_req; ++i)
+    if (c->n_rows[req_ids[i]] != N) return TTS_ERR_STATE;  // imported lineages pending: use tts_beam_fork_map
+  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, n_req, N, N, st));
   // parent map back to the host (for the length mirror and the CoW plan)
   std::vector<int32_t> parent((size_t)n_req * g.max_beams);
   TTS_CUDA(cudaMemcpyAsync(parent.data(), c->ws_parent, parent.size() * 4, cudaMemcpyDeviceToHost, st));
@@ -545,11 +549,104 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   return TTS_OK;
 }
 
+// CoW plan of a fork by parent map: the first child (in index order) of each
+// parent keeps its partially filled last page, every later child copies it
+// (ledger C6; for tts_beam_select_fork this is child j = c mod M == 0).
+static void cow_items_for(tts_ctx_t c, int req, int n_new, const int32_t* parent, std::vector<tts::AllocItem>& items) {
+  const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
+  std::vector<char> seen((size_t)g.max_beams, 0);
+  for (int cc = 0; cc < n_new; ++cc) {
+    const int par = parent[cc];
+    const int len = c->lens[(int64_t)req * g.max_beams + cc];
+    if (seen[par] && len % P) items.push_back({entry_of(g, req, cc, (len - 1) / P), 1, len % P});
+    seen[par] = 1;
+  }
+}
+
+tts_status_t tts_beam_fork_map(tts_ctx_t c, int32_t req, int32_t n_new, const int32_t* parent_h, void* stream) {
+  if (!c || !parent_h || n_new <= 0) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  const tts_config_t& g = c->cfg;
+  const int n_old = c->n_rows[req];
+  if (n_new > g.max_beams) return TTS_ERR_CAPACITY;
+  for (int i = 0; i < n_new; ++i)
+    if (parent_h[i] < 0 || parent_h[i] >= n_old || c->lens[(int64_t)req * g.max_beams + parent_h[i]] <= 0)
+      return TTS_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  int32_t reqv = req;
+  void* dreq = tts::upload(c, &reqv, 4, st, &e);
+  TTS_CUDA(e);
+  TTS_CUDA(cudaMemcpyAsync(c->ws_parent, parent_h, (size_t)n_new * 4, cudaMemcpyHostToDevice, st));
+  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, 1, n_old, n_new, st));
+  int32_t* lens = c->lens.data() + (int64_t)req * g.max_beams;
+  std::vector<int32_t> old(lens, lens + g.max_beams);
+  for (int cc = 0; cc < g.max_beams; ++cc) lens[cc] = cc < n_new ? old[parent_h[cc]] : 0;
+  std::vector<tts::AllocItem> items;
+  cow_items_for(c, req, n_new, parent_h, items);
+  if (!items.empty()) {
+    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
+  }
+  c->n_beams[req] = n_new;
+  c->n_rows[req] = n_new;
+  TTS_CUDA(cudaStreamSynchronize(st));  // parent_h is a borrowed host buffer
+  return TTS_OK;
+}
+
+tts_status_t tts_beam_select_global(tts_ctx_t c, int32_t n_global, const float* scores_all, int32_t width_m,
+                                    int32_t* parent_gid_out, void* stream) {
+  if (!c || !scores_all || !parent_gid_out) return TTS_ERR_INVALID_ARG;
+  if (n_global <= 0 || n_global > 1024 || width_m <= 0 || n_global % width_m) return TTS_ERR_INVALID_ARG;
+  TTS_CUDA(tts::launch_select_global(c, scores_all, n_global, width_m, parent_gid_out, (cudaStream_t)stream));
+  return TTS_OK;
+}
+
+tts_status_t tts_lineage_bytes(tts_ctx_t c, int32_t len, size_t* bytes_h) {
+  if (!c || !bytes_h || len < 0) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  *bytes_h = (size_t)2 * g.num_layers * len * g.num_kv_heads * g.head_dim * 2;
+  return TTS_OK;
+}
+
+tts_status_t tts_lineage_export(tts_ctx_t c, int32_t req, int32_t beam, void* buf, void* stream) {
+  if (!c || !buf) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req) || beam < 0 || beam >= c->n_rows[req]) return TTS_ERR_STATE;
+  const int len = c->lens[(int64_t)req * c->cfg.max_beams + beam];
+  TTS_CUDA(tts::launch_lineage_export(c, req, beam, len, buf, (cudaStream_t)stream));
+  return TTS_OK;
+}
+
+tts_status_t tts_lineage_import(tts_ctx_t c, int32_t req, int32_t beam, int32_t len, const void* buf, void* stream) {
+  if (!c || !buf || len <= 0) return TTS_ERR_INVALID_ARG;
+  const tts_config_t& g = c->cfg;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  if (beam < c->n_beams[req] || beam >= g.max_beams || c->lens[(int64_t)req * g.max_beams + beam] != 0)
+    return TTS_ERR_STATE;
+  const int P = g.page_size, npg = (len + P - 1) / P;
+  if (npg > g.max_pages_per_beam) return TTS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  std::vector<tts::AllocItem> items;
+  for (int i = 0; i < npg; ++i) items.push_back({entry_of(g, req, beam, i), 0, 0});
+  void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
+  TTS_CUDA(e);
+  TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, npg, st));
+  TTS_CUDA(tts::launch_lineage_import(c, req, beam, len, buf, st));
+  c->lens[(int64_t)req * g.max_beams + beam] = len;
+  c->n_rows[req] = std::max(c->n_rows[req], beam + 1);
+  return TTS_OK;
+}
+
 tts_status_t tts_block_table_release_request(tts_ctx_t c, int32_t req, void* stream) {
   if (!c) return TTS_ERR_INVALID_ARG;
   if (!installed(c, req)) return TTS_ERR_STATE;
-  TTS_CUDA(tts::launch_release(c, req, c->n_beams[req], (cudaStream_t)stream));
+  TTS_CUDA(tts::launch_release(c, req, c->n_rows[req], (cudaStream_t)stream));
   c->n_beams[req] = 0;
+  c->n_rows[req] = 0;
   std::fill(c->lens.begin() + (int64_t)req * c->cfg.max_beams,
             c->lens.begin() + (int64_t)(req + 1) * c->cfg.max_beams, 0);
   return TTS_OK;

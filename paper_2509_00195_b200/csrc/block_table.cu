@@ -253,36 +253,43 @@ __global__ void __launch_bounds__(kSelThreads) k_select(DevState s, const int32_
   (void)reqs;
 }
 
-// Fork, step A: new rows into tmp (child c <- row parent[c]); refcounts
-// recounted by -1 per old row entry and +1 per new row entry (commuting atomics).
-__global__ void k_fork_count(DevState s, const int32_t* reqs, const int32_t* parent, int N,
+// Fork, step A: new rows into tmp (child c <- old row parent[c]); refcounts
+// recounted by -1 per old-row entry and +1 per new-row entry (commuting
+// atomics).  Old rows [0, n_old), new rows [0, n_new); n_old > n_new when
+// migrated lineages were imported into spare slots (multi-GPU, a8).
+__global__ void k_fork_count(DevState s, const int32_t* reqs, const int32_t* parent, int n_old, int n_new,
                              int32_t* tmp_tables, int32_t* tmp_lens) {
   if (*(volatile int32_t*)s.status) return;
   const int call = blockIdx.y;
-  const int b = blockIdx.x;  // old row b and new row c = b
+  const int b = blockIdx.x;  // old row b and/or new row c = b
   const int req = reqs[call];
-  const int32_t par = parent[(int64_t)call * s.maxB + b];
-  const int len_old = s.lens[(int64_t)req * s.maxB + b];
-  const int len_par = s.lens[(int64_t)req * s.maxB + par];
-  const int np_old = (len_old + s.P - 1) / s.P;
-  const int np_new = (len_par + s.P - 1) / s.P;
-  const int32_t* old_row = s.tables + row_base(s, req, b);
-  const int32_t* par_row = s.tables + row_base(s, req, par);
-  int32_t* new_row = tmp_tables + row_base(s, req, b);
-  for (int i = threadIdx.x; i < np_old; i += blockDim.x) atomicSub(&s.ref[old_row[i]], 1);
-  for (int i = threadIdx.x; i < np_new; i += blockDim.x) {
-    int32_t p = par_row[i];
-    new_row[i] = p;
-    atomicAdd(&s.ref[p], 1);
+  if (b < n_old) {
+    const int len_old = s.lens[(int64_t)req * s.maxB + b];
+    const int np_old = (len_old + s.P - 1) / s.P;
+    const int32_t* old_row = s.tables + row_base(s, req, b);
+    for (int i = threadIdx.x; i < np_old; i += blockDim.x) atomicSub(&s.ref[old_row[i]], 1);
   }
-  if (threadIdx.x == 0) tmp_lens[(int64_t)req * s.maxB + b] = len_par;
+  if (b < n_new) {
+    const int32_t par = parent[(int64_t)call * s.maxB + b];
+    const int len_par = s.lens[(int64_t)req * s.maxB + par];
+    const int np_new = (len_par + s.P - 1) / s.P;
+    const int32_t* par_row = s.tables + row_base(s, req, par);
+    int32_t* new_row = tmp_tables + row_base(s, req, b);
+    for (int i = threadIdx.x; i < np_new; i += blockDim.x) {
+      int32_t p = par_row[i];
+      new_row[i] = p;
+      atomicAdd(&s.ref[p], 1);
+    }
+    if (threadIdx.x == 0) tmp_lens[(int64_t)req * s.maxB + b] = len_par;
+  }
 }
 
 // Fork, step B: release pages of the old rows whose refcount reached 0.
-__global__ void k_fork_free(DevState s, const int32_t* reqs, int N) {
+__global__ void k_fork_free(DevState s, const int32_t* reqs, int n_old) {
   if (*(volatile int32_t*)s.status) return;
   const int call = blockIdx.y;
   const int b = blockIdx.x;
+  if (b >= n_old) return;
   const int req = reqs[call];
   const int len_old = s.lens[(int64_t)req * s.maxB + b];
   const int np_old = (len_old + s.P - 1) / s.P;
@@ -293,14 +300,18 @@ __global__ void k_fork_free(DevState s, const int32_t* reqs, int N) {
   }
 }
 
-// Fork, step C: install the new rows and lengths.
-__global__ void k_fork_commit(DevState s, const int32_t* reqs, int N, const int32_t* tmp_tables,
+// Fork, step C: install the new rows and lengths; spare rows [n_new, n_old) emptied.
+__global__ void k_fork_commit(DevState s, const int32_t* reqs, int n_old, int n_new, const int32_t* tmp_tables,
                               const int32_t* tmp_lens) {
   if (*(volatile int32_t*)s.status) return;
   const int call = blockIdx.y;
   const int b = blockIdx.x;
   const int req = reqs[call];
   const int64_t li = (int64_t)req * s.maxB + b;
+  if (b >= n_new) {
+    if (b < n_old && threadIdx.x == 0) s.lens[li] = 0;
+    return;
+  }
   const int len = tmp_lens[li];
   const int np = (len + s.P - 1) / s.P;
   const int32_t* src = tmp_tables + row_base(s, req, b);
@@ -308,6 +319,41 @@ __global__ void k_fork_commit(DevState s, const int32_t* reqs, int N, const int3
   for (int i = threadIdx.x; i < np; i += blockDim.x) dst[i] = src[i];
   __syncthreads();
   if (threadIdx.x == 0) s.lens[li] = len;
+}
+
+// Lineage export (migration, a8): the beam's len tokens of every layer as a
+// contiguous bf16 buffer [2 (K, V)][L][len][Hkv][d].  One block per (token, layer).
+__global__ void k_lineage_export(DevState s, int req, int beam, int len, uint4* __restrict__ buf) {
+  if (*(volatile int32_t*)s.status) return;
+  const int t = blockIdx.x, l = blockIdx.y;
+  const int vpr = s.d / 8, n = s.Hkv * vpr;
+  const int32_t page = s.tables[row_base(s, req, beam) + t / s.P];
+  const int64_t plane = (int64_t)s.L * len * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int kh = i / vpr, e = i % vpr;
+    const int64_t src = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + t % s.P) * vpr + e;
+    const int64_t dst = (((int64_t)l * len + t) * s.Hkv + kh) * vpr + e;
+    buf[dst] = reinterpret_cast<const uint4*>(s.k_pool)[src];
+    buf[plane + dst] = reinterpret_cast<const uint4*>(s.v_pool)[src];
+  }
+}
+
+// Lineage import: write the buffer into the beam's freshly allocated pages and
+// set its length (the pages were allocated by k_alloc into the row first).
+__global__ void k_lineage_import(DevState s, int req, int beam, int len, const uint4* __restrict__ buf) {
+  if (*(volatile int32_t*)s.status) return;
+  const int t = blockIdx.x, l = blockIdx.y;
+  const int vpr = s.d / 8, n = s.Hkv * vpr;
+  const int32_t page = s.tables[row_base(s, req, beam) + t / s.P];
+  const int64_t plane = (int64_t)s.L * len * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int kh = i / vpr, e = i % vpr;
+    const int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + t % s.P) * vpr + e;
+    const int64_t src = (((int64_t)l * len + t) * s.Hkv + kh) * vpr + e;
+    reinterpret_cast<uint4*>(s.k_pool)[dst] = buf[src];
+    reinterpret_cast<uint4*>(s.v_pool)[dst] = buf[plane + src];
+  }
+  if (t == 0 && l == 0 && threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + beam] = len;
 }
 
 // Release a request: -1 per entry, then free the pages that reached 0.
@@ -436,13 +482,34 @@ cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float*
   return cudaGetLastError();
 }
 
-cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int N, cudaStream_t st) {
+cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t st) {
   DevState s = dev_state(c);
-  dim3 grid(N, n_req);
-  k_fork_count<<<grid, 128, 0, st>>>(s, reqs_d, c->ws_parent, N, c->ws_tmp_tables, c->ws_tmp_lens);
-  k_fork_free<<<grid, 128, 0, st>>>(s, reqs_d, N);
-  k_fork_commit<<<grid, 128, 0, st>>>(s, reqs_d, N, c->ws_tmp_tables, c->ws_tmp_lens);
+  dim3 grid(n_old > n_new ? n_old : n_new, n_req);
+  k_fork_count<<<grid, 128, 0, st>>>(s, reqs_d, c->ws_parent, n_old, n_new, c->ws_tmp_tables, c->ws_tmp_lens);
+  k_fork_free<<<grid, 128, 0, st>>>(s, reqs_d, n_old);
+  k_fork_commit<<<grid, 128, 0, st>>>(s, reqs_d, n_old, n_new, c->ws_tmp_tables, c->ws_tmp_lens);
   c->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t st) {
+  if (len <= 0) return cudaSuccess;
+  k_lineage_export<<<dim3(len, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len, (uint4*)buf);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t st) {
+  if (len <= 0) return cudaSuccess;
+  k_lineage_import<<<dim3(len, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len, (const uint4*)buf);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_global(Ctx* c, const float* scores_all, int N, int M, int32_t* parent_out,
+                                 cudaStream_t st) {
+  k_select<<<1, kSelThreads, 0, st>>>(dev_state(c), nullptr, scores_all, N, M, parent_out, parent_out);
+  c->launches++;
   return cudaGetLastError();
 }
 

@@ -54,6 +54,7 @@ struct Ctx {
   // host mirror of lengths / beam counts (lengths change only through the API)
   std::vector<int32_t> n_beams;  // per request, 0 = not installed
   std::vector<int32_t> lens;     // [max_requests][max_beams]
+  std::vector<int32_t> n_rows;   // per request: rows in use (>= n_beams while imported lineages wait)
   // pinned upload ring
   uint8_t* pinned = nullptr;
   cudaEvent_t ev[kUploadSlots];
@@ -102,7 +103,11 @@ cudaError_t launch_append_write(Ctx* c, const int32_t* slots_d, int n_slots, int
                                 const __nv_bfloat16* k, const __nv_bfloat16* v, cudaStream_t s);
 cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float* scores,
                           int N, int M, int32_t* parent_out, cudaStream_t s);
-cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int N, cudaStream_t s);
+cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t s);
+cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t s);
+cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t s);
+cudaError_t launch_select_global(Ctx* c, const float* scores_all, int N, int M, int32_t* parent_out,
+                                 cudaStream_t s);
 cudaError_t launch_release(Ctx* c, int req, int n_beams, cudaStream_t s);
 cudaError_t launch_stats(Ctx* c, const GroupDesc* groups_d, int n_groups, int64_t* accum,
                          int64_t logical, cudaStream_t s);

@@ -20,13 +20,26 @@ from synth import rng, workload
 from .tts import Context, TTSConfig
 
 
+def pages_per_request(cfg: workload.Config) -> int:
+    """Upper bound on the live pages of one request.  Fixed-length steps: the
+    prompt (+ CoW copies of a partial last prompt page), at most K = N/M
+    distinct survivors' segments for every finished step (later forks only
+    drop lineages), and N private segments for the current step (+1 page each
+    for a CoW'd partial page).  Variable steps: every beam's whole chain."""
+    P = cfg.P
+    if cfg.step_len > 0:
+        seg = -(-cfg.step_len // P) + 1
+        return -(-cfg.prompt // P) + cfg.N + (cfg.n_steps - 1) * cfg.K * seg + cfg.N * seg
+    return cfg.N * workload.max_pages_per_beam(cfg)
+
+
 def tts_config(cfg: workload.Config, n_req: int, num_pages: Optional[int] = None,
-               max_pages_per_beam: Optional[int] = None) -> TTSConfig:
+               max_pages_per_beam: Optional[int] = None, max_beams: Optional[int] = None) -> TTSConfig:
     mp = max_pages_per_beam or workload.max_pages_per_beam(cfg)
     if num_pages is None:
-        num_pages = cfg.num_pages or (n_req * cfg.N * mp + 64)
+        num_pages = cfg.num_pages or (n_req * pages_per_request(cfg) + 64)
     return TTSConfig(num_layers=cfg.L, num_q_heads=cfg.Hq, num_kv_heads=cfg.Hkv, head_dim=cfg.d,
-                     page_size=cfg.P, max_requests=n_req, max_beams=cfg.N, max_pages_per_beam=mp,
+                     page_size=cfg.P, max_requests=n_req, max_beams=max_beams or cfg.N, max_pages_per_beam=mp,
                      num_pages=int(num_pages))
 
 

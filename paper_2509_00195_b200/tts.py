@@ -76,6 +76,11 @@ def load() -> ctypes.CDLL:
             "tts_decode_step": [_P, _I, _P, _P, _P, _P, _P, ctypes.c_float, _P, _P],
             "tts_profile_begin": [_P],
             "tts_profile_end": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)],
+            "tts_beam_select_global": [_P, _I, _P, _I, _P, _P],
+            "tts_beam_fork_map": [_P, _I, _I, _P, _P],
+            "tts_lineage_bytes": [_P, _I, ctypes.POINTER(ctypes.c_size_t)],
+            "tts_lineage_export": [_P, _I, _I, _P, _P],
+            "tts_lineage_import": [_P, _I, _I, _I, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -237,6 +242,32 @@ class Context:
         _check(self.lib.tts_beam_select_fork(self.h, len(req_ids), _i32_host(req_ids), _ptr(scores),
                                              int(width_m), _ptr(parent_out), self.stream),
                "tts_beam_select_fork")
+
+    def tts_beam_select_global(self, scores_all, width_m, parent_gid_out):
+        _check(self.lib.tts_beam_select_global(self.h, scores_all.numel(), _ptr(scores_all), int(width_m),
+                                               _ptr(parent_gid_out), self.stream), "tts_beam_select_global")
+
+    def tts_beam_fork_map(self, req, parent_local):
+        arr = _i32_host(parent_local)
+        _check(self.lib.tts_beam_fork_map(self.h, req, len(parent_local), arr, self.stream), "tts_beam_fork_map")
+
+    def tts_lineage_bytes(self, length) -> int:
+        n = ctypes.c_size_t()
+        _check(self.lib.tts_lineage_bytes(self.h, int(length), ctypes.byref(n)), "tts_lineage_bytes")
+        return n.value
+
+    def tts_lineage_export(self, req, beam, buf):
+        _check(self.lib.tts_lineage_export(self.h, req, beam, _ptr(buf), self.stream), "tts_lineage_export")
+
+    def tts_lineage_import(self, req, beam, length, buf):
+        _check(self.lib.tts_lineage_import(self.h, req, beam, int(length), _ptr(buf), self.stream),
+               "tts_lineage_import")
+
+    def lineage_buffer(self, length) -> torch.Tensor:
+        return torch.empty(max(16, self.tts_lineage_bytes(length)), dtype=torch.uint8, device=self.device)
+
+    def sync(self):
+        torch.cuda.current_stream(self.device).synchronize()
 
     def tts_block_table_release_request(self, req):
         _check(self.lib.tts_block_table_release_request(self.h, req, self.stream),
