@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--dump-call-bytes", default="")
     ap.add_argument("--requests", type=int, default=0, help="override R of the straggler batch (C4)")
+    ap.add_argument("--tts-steps", type=int, default=0, help="override the number of TTS steps (shorter chains)")
     ap.add_argument("--pages-per-request", type=int, default=0,
                     help="page-pool budget per request (default: exact bound for fixed steps, 6000 for C4)")
     return ap.parse_args()
@@ -259,6 +260,88 @@ class Bench:
             self._chk(lib.tts_block_table_release_request(h, self.local[r], st), "release")
 
 
+class SpanBench:
+    """C5: one request whose N beams span the G ranks (n = N / G per rank).
+    Per decode iteration each rank runs append + attention on its n beams;
+    at every step end the ranks all-gather scores and lengths (NCCL), run the
+    same global selection and migrate lineages whose children changed rank
+    (paper_2509_00195_b200.dist.select_fork_global)."""
+
+    def __init__(self, cfg, world, rank, dev_index, ring=8):
+        from paper_2509_00195_b200 import build
+        build.build()
+        from paper_2509_00195_b200.runner import tts_config, Inputs
+        from paper_2509_00195_b200.tts import Context
+        self.cfg, self.world, self.rank = cfg, world, rank
+        self.nl = cfg.N // world
+        maxb = 2 * self.nl if world > 1 else cfg.N
+        pages = self.nl * workload.max_pages_per_beam(cfg) + 256  # every local lineage fully private
+        self.tcfg = tts_config(cfg, 1, num_pages=pages, max_beams=maxb)
+        self.ctx = Context(self.tcfg, dev_index)
+        self.lib, self.h, self.dev = self.ctx.lib, self.ctx.h, self.ctx.device
+        self.inp = Inputs(cfg, self.dev)
+        self.scale = ctypes.c_float(1.0 / math.sqrt(cfg.d))
+        self.batched = False
+        self.greqs = [0]
+        self.ring = []
+        for i in range(ring):
+            q = torch.randn(cfg.L, 1, maxb, cfg.Hq, cfg.d, device=self.dev).to(torch.bfloat16)
+            k = torch.randn(cfg.L, 1, maxb, cfg.Hkv, cfg.d, device=self.dev).to(torch.bfloat16)
+            v = torch.randn(cfg.L, 1, maxb, cfg.Hkv, cfg.d, device=self.dev).to(torch.bfloat16)
+            self.ring.append((q, k, v))
+        self.out = torch.empty(cfg.L, 1, maxb, cfg.Hq, cfg.d, dtype=torch.float32, device=self.dev)
+        self.prompt = self.inp.prompt_kv(0)
+        self.sched = list(workload.schedule(cfg, [0]))
+        sl = slice(rank * self.nl, (rank + 1) * self.nl)
+        self.scores = {s: self.inp.scores(0, s)[sl].contiguous() for it in self.sched for (_, s) in it.forks}
+        self.act = {}
+        self.beam_steps = sum(int(it.active[0][sl].sum()) for it in self.sched)
+        self.n_calls = len(self.sched)
+        self.ncall = 0
+        self.stream = self.ctx.stream
+        self.req = (ctypes.c_int32 * 1)(0)
+        torch.cuda.synchronize(self.dev)
+
+    def _chk(self, code, what):
+        if code != 0:
+            from paper_2509_00195_b200.tts import TTSError
+            raise TTSError(code, what)
+
+    def run_step(self, stats_accum=None, e2e=None):
+        from paper_2509_00195_b200.dist import select_fork_global
+        c, lib, h, st = self.cfg, self.lib, self.h, self.stream
+        k, v = self.prompt
+        self._chk(lib.tts_block_table_init_request(h, 0, self.nl, c.prompt, k.data_ptr(), v.data_ptr(), st), "init")
+        nr = len(self.ring)
+        for it in self.sched:
+            q, k, v = self.ring[it.t % nr]
+            if e2e is not None:
+                hq, hk, hv = e2e["ring"][it.t % nr]
+                q, k, v = e2e["q"], e2e["k"], e2e["v"]
+                q.copy_(hq, non_blocking=True)
+                k.copy_(hk, non_blocking=True)
+                v.copy_(hv, non_blocking=True)
+            self._chk(lib.tts_decode_step(h, 1, self.req, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
+                                          self.scale, self.out.data_ptr(), st), "decode_step")
+            if stats_accum is not None:
+                self._chk(lib.tts_block_table_stats(h, 1, self.req, None, stats_accum[self.ncall].data_ptr(), st),
+                          "stats")
+                self.ncall += 1
+            for (_, s) in it.forks:
+                sc = self.scores[s]
+                if e2e is not None:
+                    sc = sc.cpu().pin_memory().to(self.dev, non_blocking=True)
+                    e2e["d2h"] += c.N * 4
+                if self.world > 1:
+                    select_fork_global(self.ctx, 0, sc, c.M)
+                else:
+                    self.ctx.tts_beam_select_fork([0], sc.view(1, -1), c.M)
+        if e2e is not None:
+            e2e["last_out"].copy_(self.out, non_blocking=True)
+            e2e["d2h"] += self.out.numel() * 4
+        self._chk(lib.tts_block_table_release_request(h, 0, st), "release")
+
+
 def cpu_baseline(cfg, seconds):
     """The oracle as it stands, on a bounded sample: the first decode iterations
     of request 0 with full attention (all active beams x all layers) per
@@ -338,19 +421,28 @@ def main():
     dev = torch.device("cuda", local)
     cfg = workload.CONFIGS[args.config]
     rot = args.rotate or DEFAULT_ROTATE[args.config]
+    if args.tts_steps:
+        cfg = cfg.with_(n_steps=args.tts_steps)
     ppr = args.pages_per_request
-    if cfg.step_len == 0:
+    span = args.config == "C5"
+    if span:
+        # one request, its N beams spread over the ranks; global top-K each step
+        scaling = "strong"
+        b = SpanBench(cfg, ws, rank, local)
+        greqs = [0]
+    elif cfg.step_len == 0:
         # straggler batch: shard the R requests over ranks (request r -> rank r mod G)
         if args.requests:
             cfg = cfg.with_(R=args.requests)
         greqs = [r for r in range(cfg.R) if r % ws == rank]
         scaling = "strong"
-        ppr = ppr or 6000  # ~3x the simulated mean live pages of a C4 request
+        # page budget: runner.pages_per_request (override with --pages-per-request)
     else:
         cfg = cfg.with_(R=rot * ws)  # independent requests of the same shape, rot per rank
         greqs = [rank * rot + i for i in range(rot)]
         scaling = "weak"
-    b = Bench(cfg, greqs, local, pages_per_request=ppr)
+    if not span:
+        b = Bench(cfg, greqs, local, pages_per_request=ppr)
     st = torch.cuda.current_stream(dev)
 
     # warm-up (the first one also accumulates the unique / logical KV statistics)
@@ -358,7 +450,8 @@ def main():
     for i in range(max(args.warmup, 1)):
         b.run_step(stats_accum=per_call if i == 0 else None)
     torch.cuda.synchronize(dev)
-    assert b.ctx.tts_device_status() == 0, "device status error during warm-up"
+    st_code = b.ctx.tts_device_status()
+    assert st_code == 0, f"device status {st_code} during warm-up"
     unique_tok, logical_tok = [int(x) for x in per_call.sum(0).tolist()]
     kv_tok = 4 * cfg.Hkv * cfg.d * cfg.L  # bytes per token over all layers (bf16 K+V)
     if args.dump_call_bytes:
@@ -456,7 +549,9 @@ def main():
                        "beam_steps_per_rank_step": b.beam_steps,
                        "l2": (f"rotation over {len(greqs)} independent requests, one per call" if not b.batched
                               else "batched requests (working set >> L2)"),
-                       "parallelism": f"dp{ws} (independent requests per rank, no data-path collective)"},
+                       "parallelism": (f"beam-sharded x{ws} (one request's beams span the ranks; NCCL all-gather "
+                                       "of scores + lineage migration per step)" if span else
+                                       f"dp{ws} (independent requests per rank, no data-path collective)")},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk, "unit": "GB/s",
                          "frac": achieved_gbs / pk, "traffic": traffic, "traffic_over_algo": traffic_ratio,
                          "peak_source": pk_src,

@@ -30,7 +30,15 @@ def pages_per_request(cfg: workload.Config) -> int:
     if cfg.step_len > 0:
         seg = -(-cfg.step_len // P) + 1
         return -(-cfg.prompt // P) + cfg.N + (cfg.n_steps - 1) * cfg.K * seg + cfg.N * seg
-    return cfg.N * workload.max_pages_per_beam(cfg)
+    # variable steps (C4): every beam's pages of the current step, plus K
+    # survivors per finished step at 1.5x the step's mean length (survivors are
+    # chosen by score, not length); a pool that runs out raises the sticky
+    # TTS_ERR_OUT_OF_PAGES, it never corrupts state
+    lens = workload.step_lengths(cfg)                      # [R][S][N]
+    pages = -(-lens // P)
+    cur = (pages.sum(axis=2) + cfg.N).max(axis=1)          # [R]
+    past = (1.5 * pages.mean(axis=2) + 1).sum(axis=1) * cfg.K
+    return int(-(-cfg.prompt // P) + cfg.N + (cur + past).max())
 
 
 def tts_config(cfg: workload.Config, n_req: int, num_pages: Optional[int] = None,
