@@ -14,9 +14,9 @@
 // every beam and GQA head of the group that references it (the reuse Dynamic
 // Prefix-Aware Scheduling creates).  Consumer warps each own 16
 // query rows (bpt = 16 / G beams x G heads) and run S = Q K^T and O += P V on
-// tensor cores (bf16 in, fp32 accumulate) with an fp32 online softmax; P is
-// split hi/lo into two bf16 operands for the PV product (SURVEY ledger C14:
-// a single bf16 P fails the 2e-3 bar).  Output is fp32 (ledger C13).
+// tensor cores (bf16 Q.K, fp16 P.V with V kept in fp16 in the pool; fp32
+// accumulate) with an fp32 online softmax (SURVEY ledger C14: a bf16 P fails
+// the 2e-3 bar, fp16 P with fp16 V does not).  Output is fp32 (ledger C13).
 #include "tts_internal.cuh"
 
 namespace tts {
@@ -50,7 +50,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(bar),
       "r"(parity)
       : "memory");
@@ -95,6 +95,20 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], 
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -333,20 +347,14 @@ __global__ void __launch_bounds__((NCONS + 1) * 32)
           o[i][3] *= a1;
         }
       }
-      // P as the A operand (k = 16 tokens), split hi + lo bf16
-      uint32_t ph[4], pl[4];
-      {
-        const float pv[4][2] = {{ps[0][0], ps[0][1]}, {ps[0][2], ps[0][3]},
-                                {ps[1][0], ps[1][1]}, {ps[1][2], ps[1][3]}};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          ph[k] = pack_bf16(pv[k][0], pv[k][1]);
-          const float2 hf = unpack_bf16(ph[k]);
-          pl[k] = pack_bf16(pv[k][0] - hf.x, pv[k][1] - hf.y);
-        }
-      }
-      // Token slots >= ntok of a partially filled page hold stale data (maybe
-      // non-finite): P is 0 there, but 0 * NaN would poison O, so zero them.
+      // P as the A operand (k = 16 tokens) in fp16; V is fp16 in the pool
+      uint32_t pa[4];
+      pa[0] = pack_f16(ps[0][0], ps[0][1]);
+      pa[1] = pack_f16(ps[0][2], ps[0][3]);
+      pa[2] = pack_f16(ps[1][0], ps[1][1]);
+      pa[3] = pack_f16(ps[1][2], ps[1][3]);
+      // token slots >= ntok of a partial page are zero-filled in the pool; the
+      // mask below keeps a stale slot from ever reaching O regardless
       uint32_t vm_a = 0xffffffffu, vm_b = 0xffffffffu;
       if (ntok < kP) {
         vm_a = (2 * tq < ntok ? 0x0000ffffu : 0u) | (2 * tq + 1 < ntok ? 0xffff0000u : 0u);
@@ -360,10 +368,8 @@ __global__ void __launch_bounds__((NCONS + 1) * 32)
         v1 &= vm_b;
         v2 &= vm_a;
         v3 &= vm_b;
-        mma_bf16(o[2 * dp], ph, v0, v1);
-        mma_bf16(o[2 * dp], pl, v0, v1);
-        mma_bf16(o[2 * dp + 1], ph, v2, v3);
-        mma_bf16(o[2 * dp + 1], pl, v2, v3);
+        mma_f16(o[2 * dp], pa, v0, v1);
+        mma_f16(o[2 * dp + 1], pa, v2, v3);
       }
     }
     __syncwarp();
@@ -461,7 +467,7 @@ bool make_tensor_maps(Ctx* c) {
   CUresult r1 = enc(&c->tmap_k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->buf.k_pool, dims, strides, box,
                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  CUresult r2 = enc(&c->tmap_v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c->buf.v_pool, dims, strides, box,
+  CUresult r2 = enc(&c->tmap_v, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, c->buf.v_pool, dims, strides, box,
                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   c->tmap_ok = (r1 == CUDA_SUCCESS && r2 == CUDA_SUCCESS);
@@ -475,7 +481,7 @@ bool make_tensor_maps(Ctx* c) {
     CUresult r3 = enc(&c->tmap3_k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c->buf.k_pool, dims3, strides3, box3, es3,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CUresult r4 = enc(&c->tmap3_v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c->buf.v_pool, dims3, strides3, box3, es3,
+    CUresult r4 = enc(&c->tmap3_v, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, c->buf.v_pool, dims3, strides3, box3, es3,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     c->tmap3_ok = (r3 == CUDA_SUCCESS && r4 == CUDA_SUCCESS);

@@ -17,8 +17,9 @@
 //   softmax WG     one thread per row: tcgen05.ld S; mask rows whose beam does not
 //                  reference the page and token slots >= ntok; fp32 online softmax
 //                  with lazy rescale (O rescaled in TMEM only when the running max
-//                  grows by > 2^8); P = hi + lo bf16 (ledger C14) -> tcgen05.st over S
-//   MMA warp       O[128 x 128] += P_hi . V + P_lo . V   (A from TMEM, V MN-major)
+//                  grows by > 2^8); P in fp16 -> tcgen05.st over S
+//   MMA warp       O[128 x 128] += P . V   fp16 x fp16 (A from TMEM; V is kept in
+//                  fp16 in the pool, MN-major operand; ledger C14)
 // Each distinct page is fetched once per CTA and multiplied against all 128
 // rows: every GQA head and every beam of the tile that references it.
 // Slices of one tile form a thread-block cluster; their partial (m, l, O) are
@@ -38,28 +39,37 @@ constexpr int kNS = 6;                       // ring slots (units)
 constexpr int kTile = kP * kD * 2;           // 4 KiB: one (page, kv head) K or V tile
 constexpr int kSlot = 2 * kU * kTile;        // 16 KiB: K tiles then V tiles
 constexpr int kRing = kNS * kSlot;           // 64 KiB
-constexpr int kThreads = 256;                // warps 0-3 softmax, 4 producer, 5 MMA, 6-7 V converters
+constexpr int kThreads = 192;                // warps 0-3 softmax, 4 producer, 5 MMA
 constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
 constexpr int kSCols = kU * kP;              // 32
 
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 3 * kNS + 6;        // full, empty, vready, sfull[2], pfull[2], pv[2]
+constexpr int kNumBars = 2 * kNS + 6;        // full, empty, sfull[2], pfull[2], pv[2]
 constexpr int kOffML = kOffBar + kNumBars * 8 + 16;
 constexpr int kSmemBytes = kOffML + 2 * kRows * 4 + 1024;
 static_assert(kRing >= kRows * kD * 4, "merge area must hold a 128x128 fp32 tile");
 
 #ifdef TTS_TRACE
 __device__ long long g_trace[1024][8];
+__device__ long long g_trace2[1024][8];
 #define TTS_TR(j, ev)                                                                   \
   do {                                                                                  \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
       g_trace[(j)][(ev)] = clock64();                                                   \
   } while (0)
+#define TTS_TR2(j, ev)                                                                  \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
+      g_trace2[(j)][(ev)] = clock64();                                                  \
+  } while (0)
 #else
 #define TTS_TR(j, ev) \
   do {                \
+  } while (0)
+#define TTS_TR2(j, ev) \
+  do {                 \
   } while (0)
 #endif
 
@@ -188,6 +198,7 @@ struct AppendPlanParams {
   int4* items;
   int32_t* counts;
   const int32_t* status;
+  int32_t* status_w;
   int L, Hkv, d, maxB, maxP;
   int64_t num_pages;
 };
@@ -203,7 +214,9 @@ __global__ void __launch_bounds__(256) k_append_plan(AppendPlanParams p) {
   const int4 it = p.slots[blockIdx.x];
   const int call = it.x, req = it.y, beam = it.z, pos = it.w;
   const int vpr = p.d / 8;  // 16-B vectors per (token, kv head) row
-  const int n = p.Hkv * vpr, total = p.L * n;
+  const int n = p.Hkv * vpr;
+  const int rows = (pos % kP == 0) ? kP : 1;  // fresh page: write slot 0, zero slots 1..P-1
+  const int total = p.L * n * rows;
   const int32_t page = p.tables[((int64_t)req * p.maxB + beam) * p.maxP + pos / kP];
   // all layers at once: 4 independent 16-B copies in flight per thread
   for (int i0 = threadIdx.x; i0 < total; i0 += 4 * (int)blockDim.x) {
@@ -213,18 +226,24 @@ __global__ void __launch_bounds__(256) k_append_plan(AppendPlanParams p) {
     for (int u = 0; u < 4; ++u) {
       const int i = i0 + u * (int)blockDim.x;
       if (i < total) {
-        const int l = i / n, r2 = i % n, kh = r2 / vpr, e = r2 % vpr;
-        const int64_t src = ((((int64_t)l * p.n_call + call) * p.maxB + beam) * p.Hkv + kh) * vpr + e;
-        dst[u] = ((((int64_t)l * p.num_pages + page) * p.Hkv + kh) * kP + pos % kP) * vpr + e;
-        kv[u] = p.k_new[src];
-        vv[u] = p.v_new[src];
+        const int so = i / (p.L * n), rest = i % (p.L * n);
+        const int l = rest / n, r2 = rest % n, kh = r2 / vpr, e = r2 % vpr;
+        dst[u] = ((((int64_t)l * p.num_pages + page) * p.Hkv + kh) * kP + pos % kP + so) * vpr + e;
+        if (so == 0) {
+          const int64_t src = ((((int64_t)l * p.n_call + call) * p.maxB + beam) * p.Hkv + kh) * vpr + e;
+          kv[u] = p.k_new[src];
+          vv[u] = p.v_new[src];
+        } else {
+          kv[u] = vv[u] = make_uint4(0, 0, 0, 0);
+        }
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (i0 + u * (int)blockDim.x < total) {
+      const int i = i0 + u * (int)blockDim.x;
+      if (i < total) {
         reinterpret_cast<uint4*>(p.k_pool)[dst[u]] = kv[u];
-        reinterpret_cast<uint4*>(p.v_pool)[dst[u]] = vv[u];
+        reinterpret_cast<uint4*>(p.v_pool)[dst[u]] = i < p.L * n ? v_to_pool(vv[u], p.status_w) : vv[u];
       }
     }
   }
@@ -242,10 +261,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   float* m_s = reinterpret_cast<float*>(bp + kOffML);
   float* l_s = m_s + kRows;
-  const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_vready = b_empty + 8 * kNS,
-                 b_sfull = b_vready + 8 * kNS, b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
+  const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
   if (*(volatile int32_t*)p.status) return;
   const int split = blockIdx.x % p.splits;
   const int gidx = blockIdx.x / p.splits;
@@ -257,7 +277,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int i = 0; i < kNS; ++i) {
       bar_init(b_full + 8 * i, 1);
       bar_init(b_empty + 8 * i, 1);
-      bar_init(b_vready + 8 * i, kU);
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(b_sfull + 8 * i, 1);
@@ -312,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
 
   // this CTA's slice of the group's page list: units [u0, u1)
+  if (threadIdx.x == 0) TTS_TR(1023, 1);  // prologue done (Q in TMEM)
   const int n_items = p.counts[gidx];
   const int n_units = (n_items + kU - 1) / kU;
   const int u0 = (int)((int64_t)split * n_units / p.splits);
@@ -367,58 +387,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       meta[slot * kU] = make_int4(-1, 0, 0, 0);
       bar_arrive(b_full + 8 * slot);
     }
-  } else if (warp >= 6) {
-    // ============================ V converters ============================
-    // Warp 6 + k converts page k of each unit: bf16 -> fp16 in place (exact for
-    // |v| < 2^16; a finite |v| >= 2^16 raises the sticky TTS_ERR_UNSUPPORTED
-    // status) and zeroes token slots >= ntok of a partial page, so that PV is
-    // one fp16 x fp16 MMA per page with fp16 P (SURVEY ledger C14: fp16 P with
-    // V in fp16 stays <= 3.6e-4 row-normwise).
-    const int k = warp - 6;
-    int slot = 0;
-    uint32_t ph = 0;
-    uint32_t vmax = 0;  // running max of |v| as bf16x2 bits (per half)
-    for (int u = u0; u < u1; ++u) {
-      bar_wait(b_full + 8 * slot, ph);
-      const int4 m = meta[slot * kU + k];
-      if (m.x >= 0) {
-        uint4* vt = reinterpret_cast<uint4*>(bp + kOffRing + slot * kSlot + (kU + k) * kTile);
-        if (m.z == kP) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            uint4 v = vt[i * 32 + lane];
-            vmax = bf16x2_absmax(vmax, v.x, v.y, v.z, v.w);
-            vt[i * 32 + lane] = make_uint4(f16x2_from_bf16x2(v.x), f16x2_from_bf16x2(v.y), f16x2_from_bf16x2(v.z),
-                                           f16x2_from_bf16x2(v.w));
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int c = i * 32 + lane;  // 16-B chunk of the [2][16 tokens][128 B] tile
-            uint4 v = vt[c];
-            if (((c >> 3) & 15) < m.z) {
-              vmax = bf16x2_absmax(vmax, v.x, v.y, v.z, v.w);
-              v = make_uint4(f16x2_from_bf16x2(v.x), f16x2_from_bf16x2(v.y), f16x2_from_bf16x2(v.z),
-                             f16x2_from_bf16x2(v.w));
-            } else {
-              v = make_uint4(0, 0, 0, 0);
-            }
-            vt[c] = v;
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      }
-      __syncwarp();
-      if (lane == 0) bar_arrive(b_vready + 8 * slot);
-      if (++slot == kNS) {
-        slot = 0;
-        ph ^= 1u;
-      }
-    }
-    // finite |v| >= 2^16 (bf16 exponent field 0x8F..0xFE) does not fit fp16
-    const uint32_t e_hi = (vmax >> 23) & 0xFF, e_lo = (vmax >> 7) & 0xFF;
-    const bool big = (e_hi >= 0x8F && e_hi < 0xFF) || (e_lo >= 0x8F && e_lo < 0xFF);
-    if (__any_sync(0xffffffffu, big) && lane == 0) atomicExch(p.status, (int32_t)TTS_ERR_UNSUPPORTED);
   } else if (warp == 5) {
     // ============================ MMA issuer ============================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
@@ -470,7 +438,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_wait(b_pfull + 8 * (j & 1), (j >> 1) & 1u);
       if (lane == 0) TTS_TR(j, 2);
       const int slot = j % kNS;
-      bar_wait(b_vready + 8 * slot, (j / kNS) & 1u);  // V converted to fp16
       tc_fence_after();
       const uint32_t pa = t_s + (j & 1) * kSCols;
       const bool e = elect_one();
@@ -515,25 +482,40 @@ __global__ void __launch_bounds__(kThreads, 2)
         wm[k] = __any_sync(0xffffffffu, mem[k]);
       }
       uint32_t ph16[kSCols / 2];
+      if (r == 0) TTS_TR2(j, 0);
+#ifdef TTS_TRACE
+      if (r == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && j < 1024) g_trace2[j][7] = 0;
+#endif
       if (wm[0] || wm[1]) {
         uint32_t sr[kSCols];
         tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
         tc_wait_ld();
-        // raw scores (scale > 0 commutes with max); masked entries -> -inf
+        if (r == 0) TTS_TR2(j, 1);
+        // raw scores (scale > 0 commutes with max).  Rows not reading page k are
+        // masked once per page (row max -> -inf, exponent offset -> -inf, so
+        // their P is exactly 0); token slots >= ntok only on a partial page.
         float v[kSCols];
 #pragma unroll
-        for (int k = 0; k < kU; ++k)
+        for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
+        float mk[kU];
 #pragma unroll
-          for (int c = 0; c < kP; ++c)
-            v[k * kP + c] = (mem[k] && c < mt[k].z) ? __uint_as_float(sr[k * kP + c]) : -INFINITY;
-        float t[11];
+        for (int k = 0; k < kU; ++k) {
+          if (mt[k].x >= 0 && mt[k].z < kP) {
 #pragma unroll
-        for (int i = 0; i < 10; ++i) t[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
-        t[10] = fmaxf(v[30], v[31]);
-        t[0] = fmax3(fmax3(t[0], t[1], t[2]), fmax3(t[3], t[4], t[5]), fmax3(t[6], t[7], fmax3(t[8], t[9], t[10])));
-        const float mx = t[0] * p.scale_log2;
+            for (int c = 0; c < kP; ++c)
+              if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
+          }
+          const float* w = v + k * kP;
+          const float t0 = fmax3(w[0], w[1], w[2]), t1 = fmax3(w[3], w[4], w[5]), t2 = fmax3(w[6], w[7], w[8]);
+          const float t3 = fmax3(w[9], w[10], w[11]), t4 = fmax3(w[12], w[13], w[14]);
+          const float mxk = fmax3(fmax3(t0, t1, t2), t3, fmax3(t4, w[15], -INFINITY));
+          mk[k] = mem[k] ? mxk : -INFINITY;
+        }
+        const float mx = fmaxf(mk[0], mk[1]) * p.scale_log2;
         const bool need = mx > m_ref + 8.0f;
+        if (r == 0) TTS_TR2(j, 2);
         if (__any_sync(0xffffffffu, need) && j > 0) {
+          if (r == 0) TTS_TR2(j, 7);
           // every earlier PV product must have landed before O is rescaled in TMEM
           bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
           tc_fence_after();
@@ -551,16 +533,21 @@ __global__ void __launch_bounds__(kThreads, 2)
           l *= alpha;
         }
         if (need) m_ref = mx;
-        const float2 nm2 = make_float2(-m_ref, -m_ref);
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
         float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
           if (wm[k]) {
+            const float nm = mem[k] ? -m_ref : -INFINITY;
+            const float2 nm2 = make_float2(nm, nm);
 #pragma unroll
             for (int c = 0; c < kP; c += 2) {
               const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
+#ifdef TTS_NOEXP
+              const float a = x.x * 0.5f, b = x.y * 0.5f;
+#else
               const float a = ex2(x.x), b = ex2(x.y);
+#endif
               lacc = fadd2(lacc, make_float2(a, b));
               ph16[(k * kP + c) / 2] = pack_f16x2(a, b);
             }
@@ -570,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
         l += lacc.x + lacc.y;
+        if (r == 0) TTS_TR2(j, 3);
       } else {
 #pragma unroll
         for (int i = 0; i < kSCols / 2; ++i) ph16[i] = 0u;
@@ -577,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // P (fp16) overwrites this unit's first 16 S columns: page k at +8k
       tc_st16(t_s + lane_off + (j & 1) * kSCols, ph16);
       tc_wait_st();
+      if (r == 0) TTS_TR2(j, 4);
       tc_fence_before();
       __syncwarp();
       if (r == 0) TTS_TR(j, 6);
@@ -633,6 +622,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
 
+  if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
   if (p.splits > 1) {
     cluster_sync();
     if (warp < 4) {
@@ -687,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
   if (warp == 5) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -697,7 +688,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 #ifdef TTS_TRACE
 extern "C" int tts_debug_read_trace(long long* out_h) {
-  return (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
+  int e = (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
+  return e ? e : (int)cudaMemcpyFromSymbol(out_h + 1024 * 8, g_trace2, sizeof(g_trace2));
 }
 #endif
 
@@ -752,6 +744,7 @@ cudaError_t launch_append_plan(Ctx* c, const int32_t* slots_d, int n_slots, int 
   p.items = c->ws_items;
   p.counts = c->ws_counts;
   p.status = c->buf.status;
+  p.status_w = c->buf.status;
   p.L = c->cfg.num_layers;
   p.Hkv = c->cfg.num_kv_heads;
   p.d = c->cfg.head_dim;

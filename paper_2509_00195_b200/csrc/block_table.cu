@@ -140,47 +140,59 @@ __global__ void k_broadcast_prompt(DevState s, int req, int n_beams, int npg) {
     s.tables[row_base(s, req, b) + pg] = p;
 }
 
-// Write prompt K/V [L][prompt][Hkv][d] into the prompt pages (16-B vectors).
+// Write prompt K/V [L][prompt][Hkv][d] into the prompt pages (16-B vectors);
+// the slots after the last prompt token of a partial last page are zeroed.
 __global__ void k_write_prompt(DevState s, int req, int prompt_len, const uint4* __restrict__ k,
                                const uint4* __restrict__ v) {
   if (*(volatile int32_t*)s.status) return;
   const int vec_per_row = s.d / 8;
+  const int rem = prompt_len % s.P;
+  const int tail = rem ? s.P - rem : 0;
   const int64_t n = (int64_t)s.L * prompt_len * s.Hkv * vec_per_row;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+  const int64_t nz = (int64_t)s.L * tail * s.Hkv * vec_per_row;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + nz;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / vec_per_row;
-    int e = (int)(i % vec_per_row);
+    const bool zero = i >= n;
+    const int64_t ii = zero ? i - n : i;
+    const int span = zero ? tail : prompt_len;
+    int64_t r = ii / vec_per_row;
+    int e = (int)(ii % vec_per_row);
     int kh = (int)(r % s.Hkv);
     int64_t r2 = r / s.Hkv;
-    int j = (int)(r2 % prompt_len);
-    int l = (int)(r2 / prompt_len);
+    int j = (int)(r2 % span) + (zero ? prompt_len : 0);
+    int l = (int)(r2 / span);
     int32_t page = s.tables[row_base(s, req, 0) + j / s.P];
     int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + j % s.P) * vec_per_row + e;
-    reinterpret_cast<uint4*>(s.k_pool)[dst] = k[i];
-    reinterpret_cast<uint4*>(s.v_pool)[dst] = v[i];
+    reinterpret_cast<uint4*>(s.k_pool)[dst] = zero ? make_uint4(0, 0, 0, 0) : k[ii];
+    reinterpret_cast<uint4*>(s.v_pool)[dst] = zero ? make_uint4(0, 0, 0, 0) : v_to_pool(v[ii], s.status);
   }
 }
 
-// CoW: copy the first ntok token slots of every (layer, kv head) of src -> dst.
+// CoW: copy the first ntok token slots of every (layer, kv head) of src -> dst
+// and zero the remaining slots of dst.
 __global__ void k_cow_copy(DevState s, const CowCopy* items) {
   if (*(volatile int32_t*)s.status) return;
   CowCopy it = items[blockIdx.x];
   const int l = blockIdx.y;
   const int vec_per_row = s.d / 8;
-  const int per_head = it.ntok * vec_per_row;
+  const int per_head = s.P * vec_per_row;
   const int n = s.Hkv * per_head;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     int kh = i / per_head;
     int off = i % per_head;  // contiguous within the head's P x d slab
     int64_t src = (((int64_t)l * s.num_pages + it.src) * s.Hkv + kh) * s.P * vec_per_row + off;
     int64_t dst = (((int64_t)l * s.num_pages + it.dst) * s.Hkv + kh) * s.P * vec_per_row + off;
-    reinterpret_cast<uint4*>(s.k_pool)[dst] = reinterpret_cast<const uint4*>(s.k_pool)[src];
-    reinterpret_cast<uint4*>(s.v_pool)[dst] = reinterpret_cast<const uint4*>(s.v_pool)[src];
+    const bool copy = off < it.ntok * vec_per_row;
+    reinterpret_cast<uint4*>(s.k_pool)[dst] =
+        copy ? reinterpret_cast<const uint4*>(s.k_pool)[src] : make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(s.v_pool)[dst] =
+        copy ? reinterpret_cast<const uint4*>(s.v_pool)[src] : make_uint4(0, 0, 0, 0);
   }
 }
 
 // Append: slot items (call_idx, req, beam, pos) -> write k/v [L][n_call][maxB][Hkv][d]
-// at token pos of the beam; lens[req][beam] = pos + 1.
+// at token pos of the beam; lens[req][beam] = pos + 1.  The first token of a
+// fresh page also zeroes the page's other slots.
 __global__ void k_append_write(DevState s, const int4* __restrict__ slots, int n_call,
                                const uint4* __restrict__ k, const uint4* __restrict__ v) {
   if (*(volatile int32_t*)s.status) return;
@@ -189,13 +201,20 @@ __global__ void k_append_write(DevState s, const int4* __restrict__ slots, int n
   const int call = it.x, req = it.y, beam = it.z, pos = it.w;
   const int vec_per_row = s.d / 8;
   const int n = s.Hkv * vec_per_row;
+  const int rows = (pos % s.P == 0) ? s.P : 1;  // fresh page: write slot 0, zero slots 1..P-1
   int32_t page = s.tables[row_base(s, req, beam) + pos / s.P];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int kh = i / vec_per_row, e = i % vec_per_row;
-    int64_t src = ((((int64_t)l * n_call + call) * s.maxB + beam) * s.Hkv + kh) * vec_per_row + e;
-    int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + pos % s.P) * vec_per_row + e;
-    reinterpret_cast<uint4*>(s.k_pool)[dst] = k[src];
-    reinterpret_cast<uint4*>(s.v_pool)[dst] = v[src];
+  for (int i = threadIdx.x; i < n * rows; i += blockDim.x) {
+    const int slot_off = i / n, r2 = i % n;
+    int kh = r2 / vec_per_row, e = r2 % vec_per_row;
+    int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + pos % s.P + slot_off) * vec_per_row + e;
+    if (slot_off == 0) {
+      int64_t src = ((((int64_t)l * n_call + call) * s.maxB + beam) * s.Hkv + kh) * vec_per_row + e;
+      reinterpret_cast<uint4*>(s.k_pool)[dst] = k[src];
+      reinterpret_cast<uint4*>(s.v_pool)[dst] = v_to_pool(v[src], s.status);
+    } else {
+      reinterpret_cast<uint4*>(s.k_pool)[dst] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4*>(s.v_pool)[dst] = make_uint4(0, 0, 0, 0);
+    }
   }
   if (l == 0 && threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + beam] = pos + 1;
 }
@@ -342,7 +361,7 @@ __global__ void k_lineage_export(DevState s, int req, int beam, int len, uint4* 
 // set its length (the pages were allocated by k_alloc into the row first).
 __global__ void k_lineage_import(DevState s, int req, int beam, int len, const uint4* __restrict__ buf) {
   if (*(volatile int32_t*)s.status) return;
-  const int t = blockIdx.x, l = blockIdx.y;
+  const int t = blockIdx.x, l = blockIdx.y;  // t < ceil(len / P) * P: slots past len are zeroed
   const int vpr = s.d / 8, n = s.Hkv * vpr;
   const int32_t page = s.tables[row_base(s, req, beam) + t / s.P];
   const int64_t plane = (int64_t)s.L * len * n;
@@ -350,8 +369,8 @@ __global__ void k_lineage_import(DevState s, int req, int beam, int len, const u
     const int kh = i / vpr, e = i % vpr;
     const int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + t % s.P) * vpr + e;
     const int64_t src = (((int64_t)l * len + t) * s.Hkv + kh) * vpr + e;
-    reinterpret_cast<uint4*>(s.k_pool)[dst] = buf[src];
-    reinterpret_cast<uint4*>(s.v_pool)[dst] = buf[plane + src];
+    reinterpret_cast<uint4*>(s.k_pool)[dst] = t < len ? buf[src] : make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(s.v_pool)[dst] = t < len ? buf[plane + src] : make_uint4(0, 0, 0, 0);
   }
   if (t == 0 && l == 0 && threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + beam] = len;
 }
@@ -466,8 +485,7 @@ cudaError_t launch_append_write(Ctx* c, const int32_t* slots_d, int n_slots, int
                                 const __nv_bfloat16* k, const __nv_bfloat16* v, cudaStream_t st) {
   if (n_slots == 0) return cudaSuccess;
   dim3 grid(n_slots, c->cfg.num_layers);
-  int threads = c->cfg.num_kv_heads * c->cfg.head_dim / 8;
-  threads = threads < 32 ? 32 : threads;
+  const int threads = 128;
   k_append_write<<<grid, threads, 0, st>>>(dev_state(c), (const int4*)slots_d, n_call,
                                            (const uint4*)k, (const uint4*)v);
   c->launches++;
@@ -501,7 +519,9 @@ cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf,
 
 cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t st) {
   if (len <= 0) return cudaSuccess;
-  k_lineage_import<<<dim3(len, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len, (const uint4*)buf);
+  const int P = c->cfg.page_size;
+  k_lineage_import<<<dim3((len + P - 1) / P * P, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len,
+                                                                                  (const uint4*)buf);
   c->launches++;
   return cudaGetLastError();
 }

@@ -85,6 +85,29 @@ struct Ctx {
   int32_t* ws_counts = nullptr;  // [max_requests * max_beams]
 };
 
+// ---- pool value format --------------------------------------------------------
+// K is stored as given (bf16).  V is stored as fp16 so that the PV product runs
+// as one fp16 x fp16 tensor-core MMA with fp16 P (SURVEY ledger C14: fp16 P
+// with V in fp16 <= 3.6e-4 row-normwise).  bf16 -> fp16 is exact for
+// 2^-14 <= |v| < 2^16 (subnormal fp16 below; abs error <= 2^-25); a finite
+// |v| >= 2^16 has no fp16 value and raises the sticky TTS_ERR_UNSUPPORTED.
+// Every slot of an allocated page that holds no token is zero-filled, so no
+// kernel ever reads stale pool data.
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t u) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(u & 0xFFFF0000u)), "f"(__uint_as_float(u << 16)));
+  return r;
+}
+__device__ __forceinline__ bool bf16x2_beyond_f16(uint32_t u) {
+  const uint32_t el = (u >> 7) & 0xFF, eh = (u >> 23) & 0xFF;
+  return (el >= 0x8F && el < 0xFF) || (eh >= 0x8F && eh < 0xFF);
+}
+__device__ __forceinline__ uint4 v_to_pool(uint4 v, int32_t* status) {
+  if (bf16x2_beyond_f16(v.x) | bf16x2_beyond_f16(v.y) | bf16x2_beyond_f16(v.z) | bf16x2_beyond_f16(v.w))
+    atomicExch(status, (int32_t)TTS_ERR_UNSUPPORTED);
+  return make_uint4(bf16x2_to_f16x2(v.x), bf16x2_to_f16x2(v.y), bf16x2_to_f16x2(v.z), bf16x2_to_f16x2(v.w));
+}
+
 // Device-copy a host blob through the pinned ring; returns device pointer.
 void* upload(Ctx* c, const void* src, size_t bytes, cudaStream_t s, cudaError_t* err);
 void upload2(Ctx* c, const void* a, size_t na, const void* b, size_t nb, cudaStream_t s, cudaError_t* err,
