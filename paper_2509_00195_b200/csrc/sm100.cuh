@@ -18,7 +18,7 @@ __device__ __forceinline__ void bar_wait(uint32_t b, uint32_t par) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
       "@!p bra W_%=;\n}" ::"r"(b),
       "r"(par)
       : "memory");
