@@ -362,24 +362,39 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
   if (use_umma) {
     // 128-row tiles: balanced runs of <= floor(128/G) beams; positions split
     // across a cluster when the grid would not fill the GPU
-    const int maxb = tts::umma_max_beams(c);
-    int gb = 1;
-    for (int i = 0; i < n_req; ++i) {
-      const int N = c->n_beams[req_ids[i]];
-      const int ng = (N + maxb - 1) / maxb;
-      gb = std::max(gb, (N + ng - 1) / ng);
-    }
+    // Tile shape: the largest beam groups (most page sharing per CTA) that
+    // still put >= 3/4 of a wave (2 CTAs per SM) on the GPU; only when even
+    // single-beam groups cannot, split each tile's page list over a cluster.
+    // Measured (C2, one request per call): 4-beam groups, no split, 40 us vs
+    // 16-beam groups split 4 ways, 47 us -- the cluster merge waits on the
+    // slowest slice.
+    int maxb = tts::umma_max_beams(c);
+    if (const char* s = std::getenv("TTS_GROUP_BEAMS")) maxb = std::max(1, std::min(maxb, std::atoi(s)));
+    const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;
+    auto group_size = [&](int cap) {
+      int gb = 1;
+      for (int i = 0; i < n_req; ++i) {
+        const int N = c->n_beams[req_ids[i]];
+        const int ng = (N + cap - 1) / cap;
+        gb = std::max(gb, (N + ng - 1) / ng);
+      }
+      return gb;
+    };
+    int gb = group_size(maxb);
     plan_groups(c, n_req, req_ids, active, gb, groups);
     if (groups.empty()) return TTS_OK;
+    if (!std::getenv("TTS_GROUP_BEAMS")) {
+      while (gb > 1 && (int64_t)groups.size() * g.num_kv_heads * n_layers < want) {
+        gb = group_size((gb + 1) / 2);
+        plan_groups(c, n_req, req_ids, active, gb, groups);
+      }
+    }
     const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
-    // slices per tile (a cluster): the smallest split that puts >= 3/4 of a wave
-    // (2 CTAs per SM) on the GPU; measured on C2 / C3 shapes, longer CTAs beat
-    // extra waves because each CTA's unit pipeline has a fixed ramp
     int splits = 1;
     if (const char* s = std::getenv("TTS_SPLITS")) {
       splits = std::max(1, std::min(8, std::atoi(s)));
     } else {
-      while (splits < 8 && ctas * splits * 4 < 3ll * 2 * c->num_sms) splits *= 2;
+      while (splits < 8 && ctas * splits < want) splits *= 2;
     }
     int max_np = 0;
     for (const auto& gd : groups) max_np = std::max(max_np, gd.max_npages);

@@ -131,43 +131,55 @@ __device__ __forceinline__ void plan_group(const GroupDesc& g, int gi, const int
   }
   __syncthreads();
   int4* out = items + g.pad[0];
-  int base = 0;
-  for (int i0 = 0; i0 < npg; i0 += NW) {
-    const int i = i0 + warp;
-    // runs of equal page ids over adjacent beams (DFS order: sharers are adjacent)
-    const bool has = i < npg && lane < nb && tb[lane * ld + i] >= 0;
-    const int page = has ? tb[lane * ld + i] : -1;
-    const uint32_t hm = __ballot_sync(0xffffffffu, has);
+  // warp w owns the contiguous positions [i_lo, i_hi): pass 1 counts its runs,
+  // one block scan turns counts into offsets, pass 2 writes the items
+  const int ppw = (npg + NW - 1) / NW;
+  const int i_lo = min(npg, warp * ppw), i_hi = min(npg, i_lo + ppw);
+  auto runs_at = [&](int i, uint32_t& hm, int& page) -> uint32_t {
+    const bool has = lane < nb && tb[lane * ld + i] >= 0;
+    page = has ? tb[lane * ld + i] : -1;
+    hm = __ballot_sync(0xffffffffu, has);
     const uint32_t below = hm & ((1u << lane) - 1u);
     const int prev = below ? 31 - __clz(below) : lane;
     const int pp = __shfl_sync(0xffffffffu, page, prev);
-    const uint32_t sm = __ballot_sync(0xffffffffu, has && (below == 0 || pp != page));
-    if (lane == 0) s_cnt[warp] = __popc(sm);
-    __syncthreads();
-    if (warp == 0) {
-      const int c = lane < NW ? s_cnt[lane] : 0;
-      int x = c;
+    return __ballot_sync(0xffffffffu, has && (below == 0 || pp != page));
+  };
+  int cnt = 0;
+  for (int i = i_lo; i < i_hi; ++i) {
+    uint32_t hm;
+    int page;
+    cnt += __popc(runs_at(i, hm, page));
+  }
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (warp == 0) {
+    const int c = lane < NW ? s_cnt[lane] : 0;
+    int x = c;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      s_off[lane] = x - c;
-      if (lane == 31) s_tot = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    __syncthreads();
+    s_off[lane] = x - c;
+    if (lane == 31) s_tot = x;
+  }
+  __syncthreads();
+  int base = s_off[warp];
+  for (int i = i_lo; i < i_hi; ++i) {
+    uint32_t hm;
+    int page;
+    const uint32_t sm = runs_at(i, hm, page);
     // the run starting at lane `lane` covers the has-lanes up to the next run start
     if ((sm >> lane) & 1u) {
       const uint32_t after = sm & ~((2u << lane) - 1u);
       const int s1 = after ? __ffs(after) - 1 : 32;
       const uint32_t members = hm & (s1 >= 32 ? 0xffffffffu : ((1u << s1) - 1u)) & ~((1u << lane) - 1u);
       const int rank = __popc(sm & ((1u << lane) - 1u));
-      out[base + s_off[warp] + rank] = make_int4(page, (int)members, min(kP, s_len[lane] - i * kP), i);
+      out[base + rank] = make_int4(page, (int)members, min(kP, s_len[lane] - i * kP), i);
     }
-    base += s_tot;
-    __syncthreads();
+    base += __popc(sm);
   }
-  if (tid == 0) counts[gi] = base;
+  if (tid == 0) counts[gi] = s_tot;
 }
 
 __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ tables, int32_t* __restrict__ lens,
@@ -635,22 +647,22 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int bl = row / G;
       const bool ok = bl < g.nbeams && ((g.active >> bl) & 1u);
       const uint32_t lm = su32(m_s + row), ll = su32(l_s + row);
-      float mk[8], wk[8];
-      float M = -INFINITY;
+      // all remote loads of a step are issued before any is consumed (DSMEM
+      // latency ~200 cycles; dependent loads would serialise)
+      float mk[8], lk[8], wk[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (k < S) {
-          mk[k] = ld_dsmem_f32(mapa(lm, k));
-          M = fmaxf(M, mk[k]);
-        }
+        mk[k] = k < S ? ld_dsmem_f32(mapa(lm, k)) : -INFINITY;
+        lk[k] = k < S ? ld_dsmem_f32(mapa(ll, k)) : 0.f;
       }
+      float M = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) M = fmaxf(M, mk[k]);
       float L = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (k < S) {
-          wk[k] = exp2f(mk[k] - M);
-          L += wk[k] * ld_dsmem_f32(mapa(ll, k));
-        }
+        wk[k] = k < S ? exp2f(mk[k] - M) : 0.f;
+        L += wk[k] * lk[k];
       }
       const float inv = 1.f / L;
       float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + bl) * p.Hq +
@@ -659,16 +671,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int c = cseg * (cw / 4) + c4;
         const int pc = (c & ~7) | ((c & 7) ^ (row & 7));
         const uint32_t la = base + kOffRing + (uint32_t)(row * kD + pc * 4) * 4;
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = k < S ? ld_dsmem_f32x4(mapa(la, k)) : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          if (k < S) {
-            const float4 v = ld_dsmem_f32x4(mapa(la, k));
-            acc.x += wk[k] * v.x;
-            acc.y += wk[k] * v.y;
-            acc.z += wk[k] * v.z;
-            acc.w += wk[k] * v.w;
-          }
+          acc.x += wk[k] * v[k].x;
+          acc.y += wk[k] * v[k].y;
+          acc.z += wk[k] * v[k].z;
+          acc.w += wk[k] * v[k].w;
         }
         if (ok) *reinterpret_cast<float4*>(orow + c * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
       }
