@@ -228,9 +228,7 @@ tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_be
   std::vector<tts::AllocItem> items;
   for (int i = 0; i < npg; ++i) items.push_back({entry_of(g, req, 0, i), 0, 0});
   if (!items.empty()) {
-    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
     TTS_CUDA(tts::launch_broadcast_prompt(c, req, n_beams, npg, st));
     TTS_CUDA(tts::launch_write_prompt(c, req, prompt_len, (const __nv_bfloat16*)k_prompt,
                                       (const __nv_bfloat16*)v_prompt, st));
@@ -239,9 +237,7 @@ tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_be
   if (rem && n_beams > 1) {
     items.clear();
     for (int b = 1; b < n_beams; ++b) items.push_back({entry_of(g, req, b, npg - 1), 1, rem});
-    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
     TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
   }
   std::vector<int32_t> lens(g.max_beams, 0);
@@ -282,9 +278,7 @@ static tts_status_t append_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_i
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (!items.empty()) {
-    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
   }
   if (!slots.empty() && !deferred) {
     void* d = tts::upload(c, slots.data(), slots.size() * 4, st, &e);
@@ -306,11 +300,14 @@ tts_status_t tts_block_table_append(tts_ctx_t c, int32_t n_req, const int32_t* r
 static void prof_pair(tts_ctx_t c, cudaEvent_t* e0, cudaEvent_t* e1);
 
 // Group plan: contiguous beam runs of `gb` slots with >= 1 active beam.
+// lens_out (optional): every group beam's current length (0 = inactive), the
+// group's first at GroupDesc.pad[0].
 static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const uint8_t* active,
-                        int gb, std::vector<tts::GroupDesc>& out) {
+                        int gb, std::vector<tts::GroupDesc>& out, std::vector<int32_t>* lens_out = nullptr) {
   const tts_config_t& g = c->cfg;
   const int P = g.page_size;
   out.clear();
+  if (lens_out) lens_out->clear();
   for (int i = 0; i < n_req; ++i) {
     const int r = req_ids[i];
     const int N = c->n_beams[r];
@@ -328,15 +325,14 @@ static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const ui
         const int len = c->lens[(int64_t)r * g.max_beams + b0 + k];
         d.max_npages = std::max(d.max_npages, (len + P - 1) / P);
       }
-      if (d.active) out.push_back(d);
+      if (!d.active) continue;
+      if (lens_out) {
+        d.pad[0] = (int32_t)lens_out->size();
+        for (int k = 0; k < d.nbeams; ++k)
+          lens_out->push_back(((d.active >> k) & 1u) ? c->lens[(int64_t)r * g.max_beams + b0 + k] : 0);
+      }
+      out.push_back(d);
     }
-  }
-  // page-list capacity of each group = sum of its active beams' pages
-  int32_t off = 0;
-  for (auto& d : out) {
-    d.pad[0] = off;
-    for (int k = 0; k < d.nbeams; ++k)
-      if ((d.active >> k) & 1u) off += (c->lens[(int64_t)d.req * g.max_beams + d.beam0 + k] + P - 1) / P;
   }
 }
 
@@ -381,12 +377,13 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
       return gb;
     };
     int gb = group_size(maxb);
-    plan_groups(c, n_req, req_ids, active, gb, groups);
+    std::vector<int32_t> glens;
+    plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
     if (groups.empty()) return TTS_OK;
     if (!std::getenv("TTS_GROUP_BEAMS")) {
       while (gb > 1 && (int64_t)groups.size() * g.num_kv_heads * n_layers < want) {
         gb = group_size((gb + 1) / 2);
-        plan_groups(c, n_req, req_ids, active, gb, groups);
+        plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
       }
     }
     const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
@@ -396,27 +393,14 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
     } else {
       while (splits < 8 && ctas * splits < want) splits *= 2;
     }
-    int max_np = 0;
-    for (const auto& gd : groups) max_np = std::max(max_np, gd.max_npages);
-    void* d = nullptr;
-    void* ds = nullptr;
-    if (pending && !pending->empty()) {
-      tts::upload2(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), pending->data(), pending->size() * 4,
-                   st, &e, &d, &ds);
-      TTS_CUDA(e);
-      TTS_CUDA(tts::launch_append_plan(c, (const int32_t*)ds, (int)pending->size() / 4, n_req,
-                                       (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
-                                       (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
-    } else {
-      d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
-      TTS_CUDA(e);
-      TTS_CUDA(tts::launch_plan(c, (const tts::GroupDesc*)d, (int)groups.size(), max_np, gb, st));
-    }
+    const bool append = pending && !pending->empty();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) prof_pair(c, &e0, &e1);
     if (e0) TTS_CUDA(cudaEventRecord(e0, st));
-    TTS_CUDA(tts::launch_attention_umma(c, (const tts::GroupDesc*)d, (int)groups.size(), splits, layer_begin,
-                                        n_layers, n_req, (const __nv_bfloat16*)q, scale, out, st));
+    TTS_CUDA(tts::launch_attention_umma(c, groups.data(), (int)groups.size(), glens.data(), (int)glens.size(),
+                                        splits, layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out,
+                                        append ? (const __nv_bfloat16*)k_new : nullptr,
+                                        append ? (const __nv_bfloat16*)v_new : nullptr, st));
     if (e1) TTS_CUDA(cudaEventRecord(e1, st));
     return TTS_OK;
   }
@@ -556,9 +540,7 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
     }
   }
   if (!items.empty()) {
-    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
     TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
   }
   return TTS_OK;
@@ -601,9 +583,7 @@ tts_status_t tts_beam_fork_map(tts_ctx_t c, int32_t req, int32_t n_new, const in
   std::vector<tts::AllocItem> items;
   cow_items_for(c, req, n_new, parent_h, items);
   if (!items.empty()) {
-    void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, (int)items.size(), st));
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
     TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
   }
   c->n_beams[req] = n_new;
@@ -647,9 +627,7 @@ tts_status_t tts_lineage_import(tts_ctx_t c, int32_t req, int32_t beam, int32_t 
   cudaError_t e;
   std::vector<tts::AllocItem> items;
   for (int i = 0; i < npg; ++i) items.push_back({entry_of(g, req, beam, i), 0, 0});
-  void* d = tts::upload(c, items.data(), items.size() * sizeof(tts::AllocItem), st, &e);
-  TTS_CUDA(e);
-  TTS_CUDA(tts::launch_alloc(c, (const tts::AllocItem*)d, npg, st));
+  TTS_CUDA(tts::launch_alloc_host(c, items.data(), npg, st));
   TTS_CUDA(tts::launch_lineage_import(c, req, beam, len, buf, st));
   c->lens[(int64_t)req * g.max_beams + beam] = len;
   c->n_rows[req] = std::max(c->n_rows[req], beam + 1);

@@ -2,13 +2,19 @@
 // (tcgen05 + TMEM + TMA), sm_100a.  Same contract as attention.cu (see there
 // and include/tts.h); this is the path for head_dim 128 and 4 <= G <= 16.
 //
-// a3 (plan, k_plan): per beam group -- a run of <= floor(128/G) consecutive
-// beams of one request, in DFS order so that every shared page's beams are
-// adjacent (ledger C5) -- the ordered list of DISTINCT pages
-// of the group's block-table rows, each with its member-beam bitmask and valid
-// token count.  Computed once per call, shared by every layer and kv head.
-//
-// a4 (k_tree_umma): one CTA owns a 128-row query tile (the group's beams x the
+// One launch per call (k_tree_umma).  Per CTA, before the tile loop:
+// a2 (tts_decode_step): the call's new token of each active beam of the group,
+// for this CTA's (layer, kv head), is written into the beam's last page (V
+// converted to the pool's fp16; a fresh page's other slots zeroed).  The last
+// page of a beam is private to it (eager copy-on-write), so no other CTA reads
+// what this CTA writes.
+// a3 (plan): the ordered list of DISTINCT pages of the group's block-table rows
+// -- a run of <= floor(128/G) consecutive beams of one request in DFS order, so
+// that every shared page's beams are adjacent (ledger C5) --
+// each with its member-beam bitmask and valid-token count, built on the fly by
+// the producer warp 32 positions at a time (lane = position) and fed straight
+// into the TMA ring.
+// a4: one CTA owns a 128-row query tile (the group's beams x the
 // G query heads of one kv head) for one layer, and a contiguous, balanced
 // slice of the group's page list when the grid would not fill the GPU.
 // Per unit of two pages:
@@ -24,6 +30,9 @@
 // rows: every GQA head and every beam of the tile that references it.
 // Slices of one tile form a thread-block cluster; their partial (m, l, O) are
 // merged through distributed shared memory, never through HBM.
+#include <cstdlib>
+#include <cstring>
+
 #include "sm100.cuh"
 #include "tts_internal.cuh"
 
@@ -48,8 +57,12 @@ constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
 constexpr int kNumBars = 2 * kNS + 6;        // full, empty, sfull[2], pfull[2], pv[2]
 constexpr int kOffML = kOffBar + kNumBars * 8 + 16;
-constexpr int kSmemBytes = kOffML + 2 * kRows * 4 + 1024;
+constexpr int kScrItems = 512;               // plan scratch: W positions x <= nb runs, W * nb <= 512
+constexpr int kOffScr = kOffML + 2 * kRows * 4;
+constexpr int kOffLen = kOffScr + kScrItems * 16;
+constexpr int kSmemBytes = kOffLen + 32 * 4 + 1024;
 static_assert(kRing >= kRows * kD * 4, "merge area must hold a 128x128 fp32 tile");
+static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
 
 #ifdef TTS_TRACE
 __device__ long long g_trace[1024][8];
@@ -74,196 +87,34 @@ __device__ long long g_trace2[1024][8];
 #endif
 
 struct UParams {
-  const int32_t* lens;
+  int32_t* lens;              // device lengths: the appended beams' new length is stored
+  const int32_t* tables;
   const __nv_bfloat16* q;
   float* out;
-  const GroupDesc* groups;
-  const int4* items;
-  const int32_t* counts;
+  const GroupDesc* groups;    // device copies when the call does not fit the parameter block,
+  const int32_t* glens;       // else null (descriptors in UInline)
   int32_t* status;
-  int layer_begin, n_call, Hq, Hkv, G, maxB, splits;
+  const uint4* k_new;         // null: no append (tts_prefix_attn_decode)
+  const uint4* v_new;
+  uint4* k_pool;
+  uint4* v_pool;
+  int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits, dbg;
   int64_t num_pages;
   float scale_log2;
 };
 
-// ---------------------------------------------------------------------------
-// a3: plan.  One CTA per group, one warp per position (NT/32 positions a round).
-template <int NT>
-__device__ __forceinline__ void plan_group(const GroupDesc& g, int gi, const int32_t* __restrict__ tables,
-                                           int32_t* __restrict__ lens, int4* __restrict__ items,
-                                           int32_t* __restrict__ counts, int maxB, int maxP, int32_t* tb,
-                                           bool bump) {
-  constexpr int NW = NT / 32;
-  __shared__ int s_len[32];
-  __shared__ int s_cnt[32];
-  __shared__ int s_off[32];
-  __shared__ int s_tot;
-  const int nb = g.nbeams, npg = g.max_npages, ld = npg + 1;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < 32) {
-    const bool act = tid < nb && ((g.active >> tid) & 1u);
-    int len = act ? lens[(int64_t)g.req * maxB + g.beam0 + tid] : 0;
-    if (act && bump) {  // fused with the append: the active beams' new token
-      len += 1;
-      lens[(int64_t)g.req * maxB + g.beam0 + tid] = len;
-    }
-    s_len[tid] = len;
-  }
-  __syncthreads();
-  // the group's table rows -> smem, all loads in flight before any store
-  const int n = nb * npg;
-  for (int b0 = tid; b0 < n; b0 += 8 * NT) {
-    int v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int idx = b0 + k * NT;
-      v[k] = -1;
-      if (idx < n) {
-        const int b = idx / npg, i = idx % npg;
-        if (i * kP < s_len[b]) v[k] = tables[((int64_t)g.req * maxB + g.beam0 + b) * maxP + i];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int idx = b0 + k * NT;
-      if (idx < n) tb[(idx / npg) * ld + idx % npg] = v[k];
-    }
-  }
-  __syncthreads();
-  int4* out = items + g.pad[0];
-  // warp w owns the contiguous positions [i_lo, i_hi): pass 1 counts its runs,
-  // one block scan turns counts into offsets, pass 2 writes the items
-  const int ppw = (npg + NW - 1) / NW;
-  const int i_lo = min(npg, warp * ppw), i_hi = min(npg, i_lo + ppw);
-  auto runs_at = [&](int i, uint32_t& hm, int& page) -> uint32_t {
-    const bool has = lane < nb && tb[lane * ld + i] >= 0;
-    page = has ? tb[lane * ld + i] : -1;
-    hm = __ballot_sync(0xffffffffu, has);
-    const uint32_t below = hm & ((1u << lane) - 1u);
-    const int prev = below ? 31 - __clz(below) : lane;
-    const int pp = __shfl_sync(0xffffffffu, page, prev);
-    return __ballot_sync(0xffffffffu, has && (below == 0 || pp != page));
-  };
-  int cnt = 0;
-  for (int i = i_lo; i < i_hi; ++i) {
-    uint32_t hm;
-    int page;
-    cnt += __popc(runs_at(i, hm, page));
-  }
-  if (lane == 0) s_cnt[warp] = cnt;
-  __syncthreads();
-  if (warp == 0) {
-    const int c = lane < NW ? s_cnt[lane] : 0;
-    int x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    s_off[lane] = x - c;
-    if (lane == 31) s_tot = x;
-  }
-  __syncthreads();
-  int base = s_off[warp];
-  for (int i = i_lo; i < i_hi; ++i) {
-    uint32_t hm;
-    int page;
-    const uint32_t sm = runs_at(i, hm, page);
-    // the run starting at lane `lane` covers the has-lanes up to the next run start
-    if ((sm >> lane) & 1u) {
-      const uint32_t after = sm & ~((2u << lane) - 1u);
-      const int s1 = after ? __ffs(after) - 1 : 32;
-      const uint32_t members = hm & (s1 >= 32 ? 0xffffffffu : ((1u << s1) - 1u)) & ~((1u << lane) - 1u);
-      const int rank = __popc(sm & ((1u << lane) - 1u));
-      out[base + rank] = make_int4(page, (int)members, min(kP, s_len[lane] - i * kP), i);
-    }
-    base += __popc(sm);
-  }
-  if (tid == 0) counts[gi] = s_tot;
-}
-
-__global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ tables, int32_t* __restrict__ lens,
-                                              const GroupDesc* __restrict__ groups, int4* __restrict__ items,
-                                              int32_t* __restrict__ counts, const int32_t* status, int maxB,
-                                              int maxP) {
-  extern __shared__ int32_t tb[];  // [nbeams][npg + 1]
-  if (*(volatile const int32_t*)status) return;
-  plan_group<1024>(groups[blockIdx.x], blockIdx.x, tables, lens, items, counts, maxB, maxP, tb, false);
-}
-
-// a2 + a3 fused (tts_decode_step): blocks [0, n_slots) append one token of one
-// beam for every layer (slot item = call, req, beam, pos), blocks [n_slots,
-// n_slots + n_groups) build the attention plan and advance the lengths of the
-// group's active beams (each beam belongs to exactly one group).  The plan
-// reads only block tables (pages were allocated before this launch) and the
-// pre-append lengths, so the two roles are independent.
-struct AppendPlanParams {
-  __nv_bfloat16* k_pool;
-  __nv_bfloat16* v_pool;
-  const int32_t* tables;
-  int32_t* lens;
-  const int4* slots;
-  int n_slots, n_call;
-  const uint4* k_new;
-  const uint4* v_new;
-  const GroupDesc* groups;
-  int4* items;
-  int32_t* counts;
-  const int32_t* status;
-  int32_t* status_w;
-  int L, Hkv, d, maxB, maxP;
-  int64_t num_pages;
+// The call's descriptors in the kernel parameter block (no H2D copy on the stream)
+constexpr int kInlineGroups = 32;
+constexpr int kInlineLens = 512;
+struct UInline {
+  GroupDesc g[kInlineGroups];
+  int32_t len[kInlineLens];  // post-append length per group beam (0: inactive); GroupDesc.pad[0] = offset
 };
-
-__global__ void __launch_bounds__(256) k_append_plan(AppendPlanParams p) {
-  extern __shared__ int32_t tb[];
-  if (*(volatile const int32_t*)p.status) return;
-  if ((int)blockIdx.x >= p.n_slots) {
-    const int gi = blockIdx.x - p.n_slots;
-    plan_group<256>(p.groups[gi], gi, p.tables, p.lens, p.items, p.counts, p.maxB, p.maxP, tb, true);
-    return;
-  }
-  const int4 it = p.slots[blockIdx.x];
-  const int call = it.x, req = it.y, beam = it.z, pos = it.w;
-  const int vpr = p.d / 8;  // 16-B vectors per (token, kv head) row
-  const int n = p.Hkv * vpr;
-  const int rows = (pos % kP == 0) ? kP : 1;  // fresh page: write slot 0, zero slots 1..P-1
-  const int total = p.L * n * rows;
-  const int32_t page = p.tables[((int64_t)req * p.maxB + beam) * p.maxP + pos / kP];
-  // all layers at once: 4 independent 16-B copies in flight per thread
-  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * (int)blockDim.x) {
-    uint4 kv[4], vv[4];
-    int64_t dst[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * (int)blockDim.x;
-      if (i < total) {
-        const int so = i / (p.L * n), rest = i % (p.L * n);
-        const int l = rest / n, r2 = rest % n, kh = r2 / vpr, e = r2 % vpr;
-        dst[u] = ((((int64_t)l * p.num_pages + page) * p.Hkv + kh) * kP + pos % kP + so) * vpr + e;
-        if (so == 0) {
-          const int64_t src = ((((int64_t)l * p.n_call + call) * p.maxB + beam) * p.Hkv + kh) * vpr + e;
-          kv[u] = p.k_new[src];
-          vv[u] = p.v_new[src];
-        } else {
-          kv[u] = vv[u] = make_uint4(0, 0, 0, 0);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * (int)blockDim.x;
-      if (i < total) {
-        reinterpret_cast<uint4*>(p.k_pool)[dst[u]] = kv[u];
-        reinterpret_cast<uint4*>(p.v_pool)[dst[u]] = i < p.L * n ? v_to_pool(vv[u], p.status_w) : vv[u];
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 2)
-    k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p) {
+    k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
+                const __grid_constant__ UInline inl) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -273,17 +124,27 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   float* m_s = reinterpret_cast<float*>(bp + kOffML);
   float* l_s = m_s + kRows;
+  int4* scr = reinterpret_cast<int4*>(bp + kOffScr);
+  int* s_len = reinterpret_cast<int*>(bp + kOffLen);
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
                  b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
+  // programmatic dependent launch: everything this kernel reads may come from
+  // the previous kernel on the stream
+  if (!(p.dbg & 4)) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (*(volatile int32_t*)p.status) return;
+  if (!(p.dbg & 8)) asm volatile("griddepcontrol.launch_dependents;");
   const int split = blockIdx.x % p.splits;
   const int gidx = blockIdx.x / p.splits;
-  const GroupDesc g = p.groups[gidx];
+  const GroupDesc g = p.groups ? p.groups[gidx] : inl.g[gidx];
   const int kh = blockIdx.y, lrel = blockIdx.z, layer = p.layer_begin + lrel;
   const int G = p.G;
+  if (threadIdx.x < 32) {
+    const bool on = threadIdx.x < g.nbeams && ((g.active >> threadIdx.x) & 1u);
+    s_len[threadIdx.x] = on ? (p.groups ? p.glens[g.pad[0] + threadIdx.x] : inl.len[g.pad[0] + threadIdx.x]) : 0;
+  }
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNS; ++i) {
@@ -337,64 +198,157 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_st32(t_q + lo, h0);
     tc_st32(t_q + lo + 32, h1);
     tc_wait_st();
+    if (p.k_new && !(p.dbg & 1)) {
+      // a2: this (layer, kv head)'s new K/V row of every active beam -> slot
+      // (len-1) % P of its last page; a fresh page's slots 1..P-1 are zeroed so
+      // that masked columns never multiply stale (possibly non-finite) V
+      const int32_t* trow = p.tables + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
+      const int64_t plane = ((int64_t)layer * p.num_pages) * p.Hkv;
+      for (int w = threadIdx.x; w < g.nbeams * 16; w += 128) {
+        const int b = w >> 4, e = w & 15;
+        const int len = s_len[b];
+        if (len <= 0) continue;
+        const int pos = len - 1;
+        const int32_t page = trow[(int64_t)b * p.maxP + pos / kP];
+        const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + pos % kP) * 16 + e;
+        const int64_t src = ((((int64_t)layer * p.n_call + g.call_idx) * p.maxB + g.beam0 + b) * p.Hkv + kh) * 16 + e;
+        p.k_pool[dst] = p.k_new[src];
+        p.v_pool[dst] = v_to_pool(p.v_new[src], p.status);
+      }
+      for (int w = threadIdx.x; w < g.nbeams * (kP - 1) * 16; w += 128) {
+        const int b = w / ((kP - 1) * 16), rest = w % ((kP - 1) * 16);
+        const int len = s_len[b];
+        if (len <= 0 || (len - 1) % kP != 0) continue;
+        const int32_t page = trow[(int64_t)b * p.maxP + (len - 1) / kP];
+        const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + 1 + rest / 16) * 16 + (rest & 15);
+        p.k_pool[dst] = make_uint4(0, 0, 0, 0);
+        p.v_pool[dst] = make_uint4(0, 0, 0, 0);
+      }
+      // generic-proxy stores -> this CTA's TMA (async proxy) reads of the page
+      if (!(p.dbg & 2)) asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (kh == 0 && lrel == 0 && split == 0 && threadIdx.x < g.nbeams && s_len[threadIdx.x] > 0)
+        p.lens[(int64_t)g.req * p.maxB + g.beam0 + threadIdx.x] = s_len[threadIdx.x];
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
 
-  // this CTA's slice of the group's page list: units [u0, u1)
   if (threadIdx.x == 0) TTS_TR(1023, 1);  // prologue done (Q in TMEM)
-  const int n_items = p.counts[gidx];
-  const int n_units = (n_items + kU - 1) / kU;
-  const int u0 = (int)((int64_t)split * n_units / p.splits);
-  const int u1 = (int)((int64_t)(split + 1) * n_units / p.splits);
-  const int4* items = p.items + g.pad[0];
 
   if (warp == 4) {
-    // ============================ producer ============================
+    // ======================= producer: plan (a3) + TMA =======================
+    // Item = (page, member-beam mask, valid tokens, position), in position order
+    // and, within a position, in beam order: a run of adjacent beams (skipping
+    // beams that do not reach the position) holding the same page id is one
+    // item.  Units = consecutive item pairs; with a cluster split, this CTA
+    // takes units [u0, u1) of the group's list.
+    const int nb = g.nbeams, npg = g.max_npages;
+    const int32_t* trow = p.tables + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
+    int t[32];
+    auto load_col = [&](int i) {
+#pragma unroll
+      for (int b = 0; b < 32; ++b)
+        t[b] = (b < nb && i < npg && i * kP < s_len[b]) ? __ldg(trow + (int64_t)b * p.maxP + i) : -1;
+    };
+    auto count_runs = [&]() {
+      int c = 0, last = -1;
+#pragma unroll
+      for (int b = 0; b < 32; ++b)
+        if (t[b] >= 0) {
+          c += t[b] != last;
+          last = t[b];
+        }
+      return c;
+    };
+    int it_lo = 0, it_hi = 0x7fffffff;
+    if (p.splits > 1) {
+      int c = 0;
+      for (int i0 = 0; i0 < npg; i0 += 32) {
+        load_col(i0 + lane);
+        c += count_runs();
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      const int n_units = (c + kU - 1) / kU;
+      it_lo = (int)((int64_t)split * n_units / p.splits) * kU;
+      it_hi = min((int)((int64_t)(split + 1) * n_units / p.splits) * kU, c);
+    }
     const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
     int slot = 0;
     uint32_t ph = 0;
-    for (int ub = u0; ub < u1; ub += 32 / kU) {
-      const int it = ub * kU + lane;
-      const int4 my = (it < min(u1 * kU, n_items)) ? items[it] : make_int4(-2, 0, 0, 0);
-      const int ue = min(u1, ub + 32 / kU);
-      for (int u = ub; u < ue; ++u) {
-        int4 m[kU];
+    auto issue = [&](const int4& m0, const int4& m1) {  // lane 0
+      bar_wait(b_empty + 8 * slot, ph ^ 1u);
+      meta[slot * kU] = m0;
+      meta[slot * kU + 1] = m1;
+      const uint32_t fb = b_full + 8 * slot;
+      bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
+      const uint32_t sb = base + kOffRing + slot * kSlot;
+      const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
+      tma3d(sb, &tmk, 0, y0, 0, fb);
+      tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
+      if (m1.x >= 0) {
+        const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
+        tma3d(sb + kTile, &tmk, 0, y1, 0, fb);
+        tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+      }
+      if (++slot == kNS) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    };
+    int4 pend = make_int4(-2, 0, 0, 0);
+    bool has_pend = false;
+    int done = 0;  // items of earlier batches
+    // W positions per batch (lane < W), W * nb <= kScrItems
+    const int W = nb <= 16 ? 32 : 16;
+    if (npg > 0) load_col(lane < W ? lane : npg);
+    for (int i0 = 0; i0 < npg && done < it_hi; i0 += W) {
+      const int i = lane < W ? i0 + lane : npg;
+      const int c = count_runs();
+      int x = c;
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          const int src = (u - ub) * kU + k;
-          m[k].x = __shfl_sync(0xffffffffu, my.x, src);
-          m[k].y = __shfl_sync(0xffffffffu, my.y, src);
-          m[k].z = __shfl_sync(0xffffffffu, my.z, src);
-          m[k].w = __shfl_sync(0xffffffffu, my.w, src);
-        }
-        if (lane == 0) {
-          bar_wait(b_empty + 8 * slot, ph ^ 1u);
-          int npages = 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const int tot = __shfl_sync(0xffffffffu, x, 31);
+      int o = x - c;
+      int last = -1, s0 = 0;
+      uint32_t mem = 0;
 #pragma unroll
-          for (int k = 0; k < kU; ++k) {
-            meta[slot * kU + k] = m[k];
-            npages += m[k].x >= 0;
+      for (int b = 0; b < 32; ++b) {
+        if (t[b] >= 0) {
+          if (t[b] != last) {
+            if (last >= 0) scr[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+            last = t[b];
+            mem = 1u << b;
+            s0 = b;
+          } else {
+            mem |= 1u << b;
           }
-          const uint32_t fb = b_full + 8 * slot;
-          bar_expect(fb, (uint32_t)(npages * 2 * kTile));
-          const uint32_t sb = base + kOffRing + slot * kSlot;
-#pragma unroll
-          for (int k = 0; k < kU; ++k) {
-            if (m[k].x < 0) continue;
-            const int y = (int)((layer_rows + (int64_t)m[k].x * p.Hkv + kh) * kP);
-            tma3d(sb + k * kTile, &tmk, 0, y, 0, fb);
-            tma3d(sb + (kU + k) * kTile, &tmv, 0, y, 0, fb);
-          }
-        }
-        if (++slot == kNS) {
-          slot = 0;
-          ph ^= 1u;
         }
       }
+      if (last >= 0) scr[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+      __syncwarp();
+      if (i0 + W < npg) load_col(lane < W ? i + W : npg);  // next batch's loads in flight while lane 0 issues
+      if (lane == 0) {
+        for (int k = max(0, it_lo - done); k < tot && done + k < it_hi; ++k) {
+          const int4 m = scr[k];
+          if (has_pend) {
+            issue(pend, m);
+            has_pend = false;
+          } else {
+            pend = m;
+            has_pend = true;
+          }
+        }
+      }
+      done += tot;
+      __syncwarp();
     }
     if (lane == 0) {
+      if (has_pend) issue(pend, make_int4(-2, 0, 0, 0));
       bar_wait(b_empty + 8 * slot, ph ^ 1u);
       meta[slot * kU] = make_int4(-1, 0, 0, 0);
       bar_arrive(b_full + 8 * slot);
@@ -715,82 +669,52 @@ int umma_max_beams(const Ctx* c) {
   return std::min(32, kRows / G);
 }
 
-cudaError_t launch_plan(Ctx* c, const GroupDesc* groups_d, int n_groups, int max_npages, int max_nbeams,
-                        cudaStream_t st) {
-  const int smem = max_nbeams * (max_npages + 1) * 4;
-  static int smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    smem_set = 200 * 1024;
-  }
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  k_plan<<<n_groups, 1024, smem, st>>>(c->buf.block_tables, c->buf.seq_lens, groups_d, c->ws_items, c->ws_counts,
-                                       c->buf.status, c->cfg.max_beams, c->cfg.max_pages_per_beam);
-  c->launches++;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_append_plan(Ctx* c, const int32_t* slots_d, int n_slots, int n_call, const __nv_bfloat16* k,
-                               const __nv_bfloat16* v, const GroupDesc* groups_d, int n_groups, int max_npages,
-                               int max_nbeams, cudaStream_t st) {
-  const int smem = max_nbeams * (max_npages + 1) * 4;
-  static int smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_append_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    smem_set = 200 * 1024;
-  }
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  AppendPlanParams p;
-  p.k_pool = (__nv_bfloat16*)c->buf.k_pool;
-  p.v_pool = (__nv_bfloat16*)c->buf.v_pool;
-  p.tables = c->buf.block_tables;
-  p.lens = c->buf.seq_lens;
-  p.slots = (const int4*)slots_d;
-  p.n_slots = n_slots;
-  p.n_call = n_call;
-  p.k_new = (const uint4*)k;
-  p.v_new = (const uint4*)v;
-  p.groups = groups_d;
-  p.items = c->ws_items;
-  p.counts = c->ws_counts;
-  p.status = c->buf.status;
-  p.status_w = c->buf.status;
-  p.L = c->cfg.num_layers;
-  p.Hkv = c->cfg.num_kv_heads;
-  p.d = c->cfg.head_dim;
-  p.maxB = c->cfg.max_beams;
-  p.maxP = c->cfg.max_pages_per_beam;
-  p.num_pages = c->cfg.num_pages;
-  k_append_plan<<<n_slots + n_groups, 256, smem, st>>>(p);
-  c->launches++;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_groups, int splits, int layer_begin,
-                                  int n_layers, int n_call, const __nv_bfloat16* q, float scale, float* out,
-                                  cudaStream_t st) {
+cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
+                                  int n_lens, int splits, int layer_begin, int n_layers, int n_call,
+                                  const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
+                                  const __nv_bfloat16* v_new, cudaStream_t st) {
   UParams p;
   p.lens = c->buf.seq_lens;
+  p.tables = c->buf.block_tables;
   p.q = q;
   p.out = out;
-  p.groups = groups_d;
-  p.items = c->ws_items;
-  p.counts = c->ws_counts;
+  p.groups = nullptr;
+  p.glens = nullptr;
   p.status = c->buf.status;
+  p.k_new = (const uint4*)k_new;
+  p.v_new = (const uint4*)v_new;
+  p.k_pool = (uint4*)c->buf.k_pool;
+  p.v_pool = (uint4*)c->buf.v_pool;
   p.layer_begin = layer_begin;
   p.n_call = n_call;
   p.Hq = c->cfg.num_q_heads;
   p.Hkv = c->cfg.num_kv_heads;
   p.G = p.Hq / p.Hkv;
   p.maxB = c->cfg.max_beams;
+  p.maxP = c->cfg.max_pages_per_beam;
   p.splits = splits;
+  static const int dbg = std::getenv("TTS_DBG") ? std::atoi(std::getenv("TTS_DBG")) : 0;
+  p.dbg = dbg;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
+  UInline inl;  // host staging of the parameter block (copied by the launch)
+  if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {
+    std::memcpy(inl.g, groups_h, (size_t)n_groups * sizeof(GroupDesc));
+    std::memcpy(inl.len, lens_h, (size_t)n_lens * 4);
+  } else {
+    cudaError_t e;
+    void *dg = nullptr, *dl = nullptr;
+    upload2(c, groups_h, (size_t)n_groups * sizeof(GroupDesc), lens_h, (size_t)n_lens * 4, st, &e, &dg, &dl);
+    if (e != cudaSuccess) return e;
+    p.groups = (const GroupDesc*)dg;
+    p.glens = (const int32_t*)dl;
+  }
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(k_tree_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
+    e = cudaFuncSetAttribute(k_tree_umma, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -799,14 +723,19 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_group
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // the prologue of this launch may overlap the tail of the previous kernel;
+  // the kernel waits (griddepcontrol.wait) before touching global memory
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap3_k, c->tmap3_v, p);
+  cfg.numAttrs = no_pdl ? 1 : 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap3_k, c->tmap3_v, p, inl);
   c->launches++;
   return e;
 }

@@ -14,6 +14,8 @@
 #include <cub/block/block_scan.cuh>
 #include <cub/block/block_reduce.cuh>
 
+#include <cstring>
+
 #include "tts_internal.cuh"
 
 namespace tts {
@@ -79,8 +81,14 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 // ascending order, to the n items in item order (ledger C7).  All-or-nothing:
 // on exhaustion it sets the sticky status and changes nothing.
 constexpr int kAllocThreads = 1024;
+constexpr int kAllocInline = 64;
+struct AllocInline {
+  AllocItem it[kAllocInline];
+};
 
+// items: device list, or null when the (<= kAllocInline) items are in `inl`
 __global__ void __launch_bounds__(kAllocThreads) k_alloc(DevState s, const AllocItem* items,
+                                                         const __grid_constant__ AllocInline inl,
                                                          int n_items, int32_t* pages_out,
                                                          CowCopy* cow_out) {
   using Scan = cub::BlockScan<int, kAllocThreads>;
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kAllocThreads) k_alloc(DevState s, const Alloc
   }
   __syncthreads();
   for (int k = tid; k < n_items; k += kAllocThreads) {
-    AllocItem it = items[k];
+    const AllocItem it = items ? items[k] : inl.it[k];
     int32_t p = pages_out[k];
     int32_t old = s.tables[it.entry];
     s.tables[it.entry] = p;
@@ -451,7 +459,23 @@ cudaError_t launch_init_state(Ctx* c, cudaStream_t st) {
 
 cudaError_t launch_alloc(Ctx* c, const AllocItem* items_d, int n_items, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
-  k_alloc<<<1, kAllocThreads, 0, st>>>(dev_state(c), items_d, n_items, c->ws_pages, c->ws_cow);
+  static const AllocInline none{};
+  k_alloc<<<1, kAllocThreads, 0, st>>>(dev_state(c), items_d, none, n_items, c->ws_pages, c->ws_cow);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_alloc_host(Ctx* c, const AllocItem* items_h, int n_items, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  if (n_items > kAllocInline) {
+    cudaError_t e;
+    void* d = upload(c, items_h, (size_t)n_items * sizeof(AllocItem), st, &e);
+    if (e != cudaSuccess) return e;
+    return launch_alloc(c, (const AllocItem*)d, n_items, st);
+  }
+  AllocInline inl;
+  std::memcpy(inl.it, items_h, (size_t)n_items * sizeof(AllocItem));
+  k_alloc<<<1, kAllocThreads, 0, st>>>(dev_state(c), nullptr, inl, n_items, c->ws_pages, c->ws_cow);
   c->launches++;
   return cudaGetLastError();
 }

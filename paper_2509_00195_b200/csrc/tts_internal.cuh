@@ -31,7 +31,7 @@ struct GroupDesc {
   int32_t nbeams;      // beams in the group (<= 32)
   uint32_t active;     // bit i: beam0 + i active
   int32_t max_npages;  // max over active beams of ceil(len / P)
-  int32_t pad[2];  // pad[0]: offset of the group's page list in ws_items
+  int32_t pad[2];  // pad[0]: offset of the group's beam lengths in the call's length list
 };
 
 // Allocation item: table entry to receive a fresh page.
@@ -118,6 +118,8 @@ size_t workspace_bytes(const tts_config_t& cfg);
 // kernels (block_table.cu)
 cudaError_t launch_init_state(Ctx* c, cudaStream_t s);
 cudaError_t launch_alloc(Ctx* c, const AllocItem* items_d, int n_items, cudaStream_t s);
+// host item list: passed in the kernel parameter block when it fits (no copy on the stream)
+cudaError_t launch_alloc_host(Ctx* c, const AllocItem* items_h, int n_items, cudaStream_t s);
 cudaError_t launch_broadcast_prompt(Ctx* c, int req, int n_beams, int npg, cudaStream_t s);
 cudaError_t launch_write_prompt(Ctx* c, int req, int prompt_len, const __nv_bfloat16* k,
                                 const __nv_bfloat16* v, cudaStream_t s);
@@ -143,13 +145,13 @@ bool make_tensor_maps(Ctx* c);
 // attention_umma.cu (tcgen05 path: d = 128, 4 <= G <= 16)
 bool umma_supported(const Ctx* c);
 int umma_max_beams(const Ctx* c);
-cudaError_t launch_plan(Ctx* c, const GroupDesc* groups_d, int n_groups, int max_npages, int max_nbeams,
-                        cudaStream_t s);
-cudaError_t launch_append_plan(Ctx* c, const int32_t* slots_d, int n_slots, int n_call, const __nv_bfloat16* k,
-                               const __nv_bfloat16* v, const GroupDesc* groups_d, int n_groups, int max_npages,
-                               int max_nbeams, cudaStream_t s);
-cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_d, int n_groups, int splits,
-                                  int layer_begin, int n_layers, int n_call, const __nv_bfloat16* q,
-                                  float scale, float* out, cudaStream_t s);
+// One launch per call: a2 (append of the call's new token, when k_new != null)
+// + a3 (plan, built on the fly per CTA) + a4.  groups_h / lens_h are HOST
+// arrays (group descriptors; per group-beam post-append lengths, 0 = inactive,
+// GroupDesc.pad[0] = offset), sent in the kernel parameter block when they fit.
+cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
+                                  int n_lens, int splits, int layer_begin, int n_layers, int n_call,
+                                  const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
+                                  const __nv_bfloat16* v_new, cudaStream_t s);
 
 }  // namespace tts

@@ -30,10 +30,15 @@ def main():
     scale = ctypes.c_float(1.0 / math.sqrt(cfg.d))
     args = (ctypes.c_void_p(k.data_ptr()), ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(q.data_ptr()), scale,
             ctypes.c_void_p(out.data_ptr()), st)
-    assert lib.tts_block_table_init_request(h, 0, cfg.N, cfg.prompt, kp.data_ptr(), vp.data_ptr(), st) == 0
-    for _ in range(64):
-        assert lib.tts_decode_step(h, 1, req, None, args[0], args[1], args[2], args[3], args[4], args[5]) == 0
-    torch.cuda.synchronize()
+    def prime():
+        # same starting point for every measurement: fresh request, 64 tokens past the prompt
+        lib.tts_block_table_release_request(h, 0, st)
+        assert lib.tts_block_table_init_request(h, 0, cfg.N, cfg.prompt, kp.data_ptr(), vp.data_ptr(), st) == 0
+        for _ in range(64):
+            assert lib.tts_decode_step(h, 1, req, None, *args) == 0
+        torch.cuda.synchronize()
+
+    prime()
     if True:
         n = 48
         torch.cuda._sleep(int(2e9 // 1000 * 200))  # stall the stream ~ 0.2 s
@@ -42,6 +47,7 @@ def main():
             lib.tts_decode_step(h, 1, req, None, *args)
         host_us = (time.perf_counter() - t0) / n * 1e6
         torch.cuda.synchronize()
+        prime()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n2 = 400
         e0.record()
@@ -50,11 +56,26 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         dev_us = e0.elapsed_time(e1) / n2 * 1e3
+        prime()
         ctx.tts_profile_begin()
+        e0.record()
         for _ in range(n2):
             lib.tts_decode_step(h, 1, req, None, *args)
+        e1.record()
         ms, cnt = ctx.tts_profile_end()
+        torch.cuda.synchronize()
+        print(f"{name}: with per-launch events: device {e0.elapsed_time(e1) / n2 * 1e3:.1f} us/call")
         attn_us = ms / max(cnt, 1) * 1e3
+        # attention only (no append): same positions, kernel without a2
+        qa = ctypes.c_void_p(q.data_ptr())
+        prime()
+        e0.record()
+        for _ in range(n2):
+            lib.tts_prefix_attn_decode(h, 0, cfg.L, 1, req, None, qa, scale, args[4], st)
+        e1.record()
+        torch.cuda.synchronize()
+        attn_only_us = e0.elapsed_time(e1) / n2 * 1e3
+    print(f"{name}: attention-only (no append) {attn_only_us:.1f} us/call")
     print(f"{name}: host enqueue {host_us:.1f} us/call, device {dev_us:.1f} us/call, attention {attn_us:.1f} us/call "
           f"(other {dev_us - attn_us:.1f})")
 
