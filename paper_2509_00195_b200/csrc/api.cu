@@ -364,6 +364,13 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
     // Measured (C2, one request per call): 4-beam groups, no split, 40 us vs
     // 16-beam groups split 4 ways, 47 us -- the cluster merge waits on the
     // slowest slice.
+    // Tile shape: the largest beam groups (most page sharing per CTA) that
+    // still put >= 3/4 of a wave (2 CTAs per SM) on the GPU; only when even
+    // single-beam groups cannot, split each tile's page list over a cluster.
+    // Measured: C2 (16 beams, one request per call) 4-beam groups, no split,
+    // 40 us vs 16-beam groups split 4 ways, 47 us (the cluster merge waits on
+    // the slowest slice); C3 (64 beams) 16-beam groups (448 CTAs) beat the
+    // better-quantised 13-beam groups (560 CTAs) by 3%.
     int maxb = tts::umma_max_beams(c);
     if (const char* s = std::getenv("TTS_GROUP_BEAMS")) maxb = std::max(1, std::min(maxb, std::atoi(s)));
     const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;

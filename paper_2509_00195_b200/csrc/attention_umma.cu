@@ -55,7 +55,7 @@ constexpr int kSCols = kU * kP;              // 32
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 6;        // full, empty, sfull[2], pfull[2], pv[2]
+constexpr int kNumBars = 2 * kNS + 8;        // full, empty, sfull[2], pfull[2], pv[2], qready, append
 constexpr int kOffML = kOffBar + kNumBars * 8 + 16;
 constexpr int kScrItems = 512;               // plan scratch: W positions x <= nb runs, W * nb <= 512
 constexpr int kOffScr = kOffML + 2 * kRows * 4;
@@ -86,6 +86,11 @@ __device__ long long g_trace2[1024][8];
   } while (0)
 #endif
 
+template <int N>
+struct IntTag {
+  static constexpr int value = N;
+};
+
 struct UParams {
   int32_t* lens;              // device lengths: the appended beams' new length is stored
   const int32_t* tables;
@@ -98,7 +103,8 @@ struct UParams {
   const uint4* v_new;
   uint4* k_pool;
   uint4* v_pool;
-  int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits, dbg;
+  int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits;
+  int copies;                 // row copies R requested (1, 2, 4; reduced to what the group's rows allow)
   int64_t num_pages;
   float scale_log2;
 };
@@ -127,15 +133,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   int4* scr = reinterpret_cast<int4*>(bp + kOffScr);
   int* s_len = reinterpret_cast<int*>(bp + kOffLen);
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16;
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_append = b_qready + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
   // programmatic dependent launch: everything this kernel reads may come from
   // the previous kernel on the stream
-  if (!(p.dbg & 4)) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (*(volatile int32_t*)p.status) return;
-  if (!(p.dbg & 8)) asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int split = blockIdx.x % p.splits;
   const int gidx = blockIdx.x / p.splits;
   const GroupDesc g = p.groups ? p.groups[gidx] : inl.g[gidx];
@@ -156,6 +162,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_init(b_pfull + 8 * i, 4);
       bar_init(b_pv + 8 * i, 1);
     }
+    bar_init(b_qready, 4);
+    bar_init(b_append, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -163,15 +171,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // rows of the tile: r -> (beam g.beam0 + r / G, q head kh*G + r % G)
+  // Rows of the tile.  The group's nrows = nbeams x G query rows are placed
+  // R = 128 / RS times (RS = 32, 64 or 128 lanes per copy, the smallest that
+  // holds them): copy `rep` (lanes [rep*RS, (rep+1)*RS)) owns columns
+  // [rep*32/R, (rep+1)*32/R) of every 32-column unit, so a small group's
+  // softmax work is spread over all four lane quadrants (warps) instead of
+  // one; the R partial states of a row are merged in the epilogue like a
+  // split-KV merge.  Row br of a copy -> (beam g.beam0 + br / G, q head kh*G + br % G).
+  const int nrows = g.nbeams * G;
+  int R = p.copies;
+  while (R > 1 && nrows > kRows / R) R >>= 1;
+  const int RS = kRows / R;
   const int r = threadIdx.x;
-  const int rbl = r / G;
-  const bool rvalid = warp < 4 && rbl < g.nbeams && ((g.active >> rbl) & 1u);
+  const int rep = r / RS, br = r % RS;
+  const int rbl = br / G;
+  const bool rvalid = warp < 4 && br < nrows && ((g.active >> rbl) & 1u);
   uint32_t qv[64];  // this thread's query row (bf16 pairs), loaded before the TMEM handshake
   if (warp < 4) {
     const uint4* src = reinterpret_cast<const uint4*>(
         p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (rvalid ? rbl : 0)) * p.Hq + kh * G +
-               r % G) * kD);
+               (rvalid ? br % G : 0)) * kD);
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const uint4 v = rvalid ? src[c] : make_uint4(0, 0, 0, 0);
@@ -198,7 +217,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_st32(t_q + lo, h0);
     tc_st32(t_q + lo + 32, h1);
     tc_wait_st();
-    if (p.k_new && !(p.dbg & 1)) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) bar_arrive(b_qready);  // the MMA warp may start S = Q K^T
+    if (p.k_new) {
       // a2: this (layer, kv head)'s new K/V row of every active beam -> slot
       // (len-1) % P of its last page; a fresh page's slots 1..P-1 are zeroed so
       // that masked columns never multiply stale (possibly non-finite) V
@@ -225,14 +247,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         p.v_pool[dst] = make_uint4(0, 0, 0, 0);
       }
       // generic-proxy stores -> this CTA's TMA (async proxy) reads of the page
-      if (!(p.dbg & 2)) asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       if (kh == 0 && lrel == 0 && split == 0 && threadIdx.x < g.nbeams && s_len[threadIdx.x] > 0)
         p.lens[(int64_t)g.req * p.maxB + g.beam0 + threadIdx.x] = s_len[threadIdx.x];
     }
+    __syncwarp();
+    if (lane == 0) bar_arrive(b_append);  // the producer may load the beams' last pages
   }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (threadIdx.x == 0) TTS_TR(1023, 1);  // prologue done (Q in TMEM)
 
@@ -284,12 +305,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t fb = b_full + 8 * slot;
       bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
       const uint32_t sb = base + kOffRing + slot * kSlot;
+      // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
+      // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
       const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
-      tma3d(sb, &tmk, 0, y0, 0, fb);
+      tma2d(sb, &tmk, 0, y0, fb);
+      tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
       tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
       if (m1.x >= 0) {
         const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
-        tma3d(sb + kTile, &tmk, 0, y1, 0, fb);
+        tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
+        tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
         tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
       }
       if (++slot == kNS) {
@@ -297,6 +322,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         ph ^= 1u;
       }
     };
+    // the first position holding a page this CTA appended to: TMA of it (and
+    // of everything after it) waits for the append stores of warps 0-3
+    int p_min = 0x7fffffff;
+    if (p.k_new)
+      for (int b = 0; b < nb; ++b)
+        if (s_len[b] > 0) p_min = min(p_min, (s_len[b] - 1) / kP);
+    bool app_wait = p_min != 0x7fffffff;
     int4 pend = make_int4(-2, 0, 0, 0);
     bool has_pend = false;
     int done = 0;  // items of earlier batches
@@ -335,6 +367,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (lane == 0) {
         for (int k = max(0, it_lo - done); k < tot && done + k < it_hi; ++k) {
           const int4 m = scr[k];
+          if (app_wait && m.w >= p_min) {
+            bar_wait(b_append, 0);
+            app_wait = false;
+          }
           if (has_pend) {
             issue(pend, m);
             has_pend = false;
@@ -357,27 +393,26 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ============================ MMA issuer ============================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
     // elected lane issues the tcgen05 instructions.
-    constexpr uint32_t id_s = idesc_bf16(kRows, kP, false);
+    constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
     constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
     const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);    // K tiles: K-major SW128
     const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
     auto issue_s = [&](int j) {
+      // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
+      // absent second page leaves columns 16..31 undefined; they are masked)
       const int slot = j % kNS;
-      const bool e = elect_one();
+      const uint32_t sd = t_s + (j & 1) * kSCols;
+      const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
+      if (elect_one()) {
 #pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        if (meta[slot * kU + k].x < 0) continue;
-        const uint32_t sd = t_s + (j & 1) * kSCols + k * kP;
-        const uint64_t dk = dk0 + (uint64_t)((slot * kSlot + k * kTile) >> 4);
-        if (e) {
-#pragma unroll
-          for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * 2048 + (ks & 3) * 32) >> 4), id_s, ks > 0);
-        }
+        for (int ks = 0; ks < kD / 16; ++ks)
+          mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s,
+                 ks > 0);
+        tc_commit(b_sfull + 8 * (j & 1));
       }
-      if (e) tc_commit(b_sfull + 8 * (j & 1));
       __syncwarp();
     };
+    bar_wait(b_qready, 0);  // Q in TMEM
     bar_wait(b_full, 0);
     tc_fence_after();
     bool done = meta[0].x == -1;
@@ -400,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncwarp();
       } else {
         issue_s(j + 1);
+        if (lane == 0) TTS_TR(j, 7);
       }
       bar_wait(b_pfull + 8 * (j & 1), (j >> 1) & 1u);
       if (lane == 0) TTS_TR(j, 2);
@@ -429,113 +465,143 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     float m_ref = -1e30f, l = 0.f;
     int j = 0;
-    for (;; ++j) {
-      if (r == 0) TTS_TR(j, 4);
-      bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
-      if (r == 0) TTS_TR(j, 5);
-      tc_fence_after();
-      const int slot = j % kNS;
-      int4 mt[kU];
+    auto loop = [&](auto cw_tag) {
+      constexpr int CW = decltype(cw_tag)::value;  // columns of every unit this copy owns
+      constexpr int PW = CW < kP ? CW : kP;        // of which per page
+      constexpr int NPG = CW / PW;                 // pages they touch (2 or 1)
+      const int c0 = rep * CW;                     // first owned column of the unit
+      const int kk0 = c0 / kP, t0 = c0 % kP;       // its page and token slot
+      for (;; ++j) {
+        if (r == 0) TTS_TR(j, 4);
+        bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
+        if (r == 0) TTS_TR(j, 5);
+        tc_fence_after();
+        const int slot = j % kNS;
+        if (meta[slot * kU].x == -1) break;
+        int4 mt[NPG];
+        bool mem[NPG], wm[NPG];
+        bool wany = false;
 #pragma unroll
-      for (int k = 0; k < kU; ++k) mt[k] = meta[slot * kU + k];
-      if (mt[0].x == -1) break;
-      // warp-uniform page membership: a warp none of whose rows reads a page
-      // skips its exponentials (P = 0 there); most private pages touch 1 warp
-      bool mem[kU], wm[kU];
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
-        wm[k] = __any_sync(0xffffffffu, mem[k]);
-      }
-      uint32_t ph16[kSCols / 2];
-      if (r == 0) TTS_TR2(j, 0);
-#ifdef TTS_TRACE
-      if (r == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && j < 1024) g_trace2[j][7] = 0;
-#endif
-      if (wm[0] || wm[1]) {
-        uint32_t sr[kSCols];
-        tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
-        tc_wait_ld();
-        if (r == 0) TTS_TR2(j, 1);
-        // raw scores (scale > 0 commutes with max).  Rows not reading page k are
-        // masked once per page (row max -> -inf, exponent offset -> -inf, so
-        // their P is exactly 0); token slots >= ntok only on a partial page.
-        float v[kSCols];
-#pragma unroll
-        for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
-        float mk[kU];
-#pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          if (mt[k].x >= 0 && mt[k].z < kP) {
-#pragma unroll
-            for (int c = 0; c < kP; ++c)
-              if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
-          }
-          const float* w = v + k * kP;
-          const float t0 = fmax3(w[0], w[1], w[2]), t1 = fmax3(w[3], w[4], w[5]), t2 = fmax3(w[6], w[7], w[8]);
-          const float t3 = fmax3(w[9], w[10], w[11]), t4 = fmax3(w[12], w[13], w[14]);
-          const float mxk = fmax3(fmax3(t0, t1, t2), t3, fmax3(t4, w[15], -INFINITY));
-          mk[k] = mem[k] ? mxk : -INFINITY;
+        for (int k = 0; k < NPG; ++k) {
+          mt[k] = meta[slot * kU + kk0 + k];
+          // warp-uniform page membership: a warp none of whose rows reads a
+          // page skips its exponentials (P = 0 there)
+          mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
+          wm[k] = __any_sync(0xffffffffu, mem[k]);
+          wany |= wm[k];
         }
-        const float mx = fmaxf(mk[0], mk[1]) * p.scale_log2;
-        const bool need = mx > m_ref + 8.0f;
-        if (r == 0) TTS_TR2(j, 2);
-        if (__any_sync(0xffffffffu, need) && j > 0) {
-          if (r == 0) TTS_TR2(j, 7);
-          // every earlier PV product must have landed before O is rescaled in TMEM
-          bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
-          tc_fence_after();
-          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
-#pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t o[32];
-            tc_ld32(t_o + lane_off + ch * 32, o);
+        uint32_t pk[CW / 2];
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) pk[i] = 0u;
+        if (wany) {
+          float v[CW];
+          {
+            uint32_t sr[CW];
+            const uint32_t ta = t_s + lane_off + (j & 1) * kSCols + c0;
+            if constexpr (CW == 32) {
+              tc_ld32(ta, sr);
+            } else if constexpr (CW == 16) {
+              tc_ld16(ta, sr);
+            } else {
+              tc_ld8(ta, sr);
+            }
             tc_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tc_st32(t_o + lane_off + ch * 32, o);
+            for (int i = 0; i < CW; ++i) v[i] = __uint_as_float(sr[i]);
           }
-          tc_wait_st();
-          l *= alpha;
-        }
-        if (need) m_ref = mx;
-        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-        float2 lacc = make_float2(0.f, 0.f);
+          // raw scores (scale > 0 commutes with max); rows not reading page k
+          // are masked once per page (max -> -inf, exponent offset -> -inf, so
+          // P is exactly 0); token slots >= ntok only on a partial page
+          float mx = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          if (wm[k]) {
-            const float nm = mem[k] ? -m_ref : -INFINITY;
-            const float2 nm2 = make_float2(nm, nm);
+          for (int k = 0; k < NPG; ++k) {
+            if (mt[k].x >= 0 && mt[k].z < t0 + PW) {
 #pragma unroll
-            for (int c = 0; c < kP; c += 2) {
-              const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
-#ifdef TTS_NOEXP
-              const float a = x.x * 0.5f, b = x.y * 0.5f;
-#else
-              const float a = ex2(x.x), b = ex2(x.y);
-#endif
-              lacc = fadd2(lacc, make_float2(a, b));
-              ph16[(k * kP + c) / 2] = pack_f16x2(a, b);
+              for (int c = 0; c < PW; ++c)
+                if (t0 + c >= mt[k].z) v[k * PW + c] = -INFINITY;
             }
-          } else {
+            const float* w = v + k * PW;
+            float mk = fmax3(w[0], w[1], w[2]);
 #pragma unroll
-            for (int c = 0; c < kP; c += 2) ph16[(k * kP + c) / 2] = 0u;
+            for (int c = 3; c + 1 < PW; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
+            if constexpr (PW % 2 == 0) mk = fmaxf(mk, w[PW - 1]);
+            mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
+          }
+          mx *= p.scale_log2;
+          const bool need = mx > m_ref + 8.0f;
+          if (__any_sync(0xffffffffu, need) && j > 0) {
+            if (r == 0) TTS_TR2(j, 7);
+            // every earlier PV product must have landed before O is rescaled in TMEM
+            bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
+            tc_fence_after();
+            const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+              uint32_t o[32];
+              tc_ld32(t_o + lane_off + ch * 32, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tc_st32(t_o + lane_off + ch * 32, o);
+            }
+            tc_wait_st();
+            l *= alpha;
+          }
+          if (need) m_ref = mx;
+          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+          float2 lacc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < NPG; ++k) {
+            if (wm[k]) {
+              const float nm = mem[k] ? -m_ref : -INFINITY;
+              const float2 nm2 = make_float2(nm, nm);
+#pragma unroll
+              for (int c = 0; c < PW; c += 2) {
+                const float2 x = ffma2(make_float2(v[k * PW + c], v[k * PW + c + 1]), sc2, nm2);
+                const float a = ex2(x.x), b = ex2(x.y);
+                lacc = fadd2(lacc, make_float2(a, b));
+                pk[(k * PW + c) / 2] = pack_f16x2(a, b);
+              }
+            }
+          }
+          l += lacc.x + lacc.y;
+        }
+        // P (fp16) over the unit's first 16 S columns (value c at column c/2):
+        // this copy's block [c0/2, c0/2 + CW/2), zeros in the other copies' blocks
+        const uint32_t tp = t_s + lane_off + (j & 1) * kSCols;
+        if constexpr (CW == 32) {
+          tc_st16(tp, pk);
+        } else if constexpr (CW == 16) {
+#pragma unroll
+          for (int bk = 0; bk < 2; ++bk) {
+            uint32_t d[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[i] = rep == bk ? pk[i] : 0u;
+            tc_st8(tp + bk * 8, d);
+          }
+        } else {
+#pragma unroll
+          for (int bk = 0; bk < 4; ++bk) {
+            uint32_t d[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = rep == bk ? pk[i] : 0u;
+            tc_st4(tp + bk * 4, d);
           }
         }
-        l += lacc.x + lacc.y;
-        if (r == 0) TTS_TR2(j, 3);
-      } else {
-#pragma unroll
-        for (int i = 0; i < kSCols / 2; ++i) ph16[i] = 0u;
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (r == 0) TTS_TR(j, 6);
+        if (lane == 0) TTS_TR2(j, warp);
+        if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
       }
-      // P (fp16) overwrites this unit's first 16 S columns: page k at +8k
-      tc_st16(t_s + lane_off + (j & 1) * kSCols, ph16);
-      tc_wait_st();
-      if (r == 0) TTS_TR2(j, 4);
-      tc_fence_before();
-      __syncwarp();
-      if (r == 0) TTS_TR(j, 6);
-      if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
+    };
+    if (R == 4) {
+      loop(IntTag<8>{});
+    } else if (R == 2) {
+      loop(IntTag<16>{});
+    } else {
+      loop(IntTag<32>{});
     }
     const int n_done = j;
     // ---------------- epilogue ----------------
@@ -543,11 +609,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_wait(b_pv + 8 * ((n_done - 1) & 1), ((n_done - 1) >> 1) & 1u);
       tc_fence_after();
     }
-    if (p.splits == 1) {
+    float* op = reinterpret_cast<float*>(bp + kOffRing);  // the ring is idle now
+    auto swz = [](int row, int c) { return (c & ~7) | ((c & 7) ^ (row & 7)); };  // 16-B chunk c of a row
+    if (R == 1 && p.splits == 1) {
       if (n_done > 0) {
         const float inv = 1.f / l;
         float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq +
-                               kh * G + r % G) * kD;
+                               kh * G + br % G) * kD;
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t o[32];
@@ -563,8 +631,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     } else {
-      // partial state -> smem (16-B chunks swizzled by row), merged across the cluster
-      float* op = reinterpret_cast<float*>(bp + kOffRing);
+      // this copy's state -> smem, rescaled to the row's max over the R copies
+      m_s[r] = m_ref;
+      if (R > 1) asm volatile("bar.sync 1, 128;" ::: "memory");
+      float M = m_ref;
+      for (int k = 0; k < R; ++k) M = fmaxf(M, m_s[br + k * RS]);
+      const float wgt = R > 1 ? exp2f(m_ref - M) : 1.f;
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t o[32];
@@ -578,13 +650,66 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
           const int c = ch * 8 + q4;
-          const int pc = (c & ~7) | ((c & 7) ^ (r & 7));
-          *reinterpret_cast<uint4*>(op + r * kD + pc * 4) =
-              make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+          *reinterpret_cast<float4*>(op + r * kD + swz(r, c) * 4) =
+              make_float4(__uint_as_float(o[4 * q4]) * wgt, __uint_as_float(o[4 * q4 + 1]) * wgt,
+                          __uint_as_float(o[4 * q4 + 2]) * wgt, __uint_as_float(o[4 * q4 + 3]) * wgt);
         }
       }
-      m_s[r] = m_ref;
-      l_s[r] = l;
+      if (R > 1) {
+        l_s[r] = l * wgt;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // the R copies of base row b2 summed by R threads, 128 / R columns each
+        const int b2 = r / R, cs = r % R;
+        const int nc4 = (kD / 4) / R;
+        float Mb = -INFINITY, Lb = 0.f;
+        for (int k = 0; k < R; ++k) {
+          Mb = fmaxf(Mb, m_s[b2 + k * RS]);
+          Lb += l_s[b2 + k * RS];
+        }
+        float4 acc[16];
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4) {
+          acc[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (c4 < nc4) {
+            const int c = cs * nc4 + c4;
+            for (int k = 0; k < R; ++k) {
+              const int rr = b2 + k * RS;
+              const float4 x = *reinterpret_cast<const float4*>(op + rr * kD + swz(rr, c) * 4);
+              acc[c4].x += x.x;
+              acc[c4].y += x.y;
+              acc[c4].z += x.z;
+              acc[c4].w += x.w;
+            }
+          }
+        }
+        const int bl2 = b2 / G;
+        const bool ok2 = b2 < nrows && ((g.active >> bl2) & 1u);
+        if (p.splits == 1) {
+          if (ok2 && n_done > 0) {
+            const float inv = 1.f / Lb;
+            float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + bl2) * p.Hq +
+                                   kh * G + b2 % G) * kD;
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4)
+              if (c4 < nc4)
+                *reinterpret_cast<float4*>(orow + (cs * nc4 + c4) * 4) =
+                    make_float4(acc[c4].x * inv, acc[c4].y * inv, acc[c4].z * inv, acc[c4].w * inv);
+          }
+        } else {
+          // merged partial of base row b2 -> row b2 (only this thread touches
+          // its column slice of row b2) for the cluster merge
+#pragma unroll
+          for (int c4 = 0; c4 < 16; ++c4)
+            if (c4 < nc4) *reinterpret_cast<float4*>(op + b2 * kD + swz(b2, cs * nc4 + c4) * 4) = acc[c4];
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (cs == 0) {
+            m_s[b2] = Mb;
+            l_s[b2] = Lb;
+          }
+        }
+      } else {
+        l_s[r] = l;
+      }
     }
   }
 
@@ -593,13 +718,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     cluster_sync();
     if (warp < 4) {
       const int S = p.splits;
-      const int rpc = kRows / S;
+      const int rpc = RS / S;  // base rows merged by this CTA
       const int tpr = 128 / rpc;
       const int row = split * rpc + threadIdx.x / tpr;
       const int cseg = threadIdx.x % tpr;
       const int cw = kD / tpr;
       const int bl = row / G;
-      const bool ok = bl < g.nbeams && ((g.active >> bl) & 1u);
+      const bool ok = row < nrows && ((g.active >> bl) & 1u);
       const uint32_t lm = su32(m_s + row), ll = su32(l_s + row);
       // all remote loads of a step are issued before any is consumed (DSMEM
       // latency ~200 cycles; dependent loads would serialise)
@@ -661,7 +786,7 @@ extern "C" int tts_debug_read_trace(long long* out_h) {
 
 bool umma_supported(const Ctx* c) {
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
-  return c->cfg.head_dim == kD && c->cfg.page_size == kP && G >= 4 && G <= 16 && c->tmap3_ok;
+  return c->cfg.head_dim == kD && c->cfg.page_size == kP && G >= 4 && G <= 16 && c->tmap3_ok && c->tmap_ok;
 }
 
 int umma_max_beams(const Ctx* c) {
@@ -693,8 +818,11 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.maxB = c->cfg.max_beams;
   p.maxP = c->cfg.max_pages_per_beam;
   p.splits = splits;
-  static const int dbg = std::getenv("TTS_DBG") ? std::atoi(std::getenv("TTS_DBG")) : 0;
-  p.dbg = dbg;
+  // row copies (see the kernel): measured neutral-to-slower on C2 (the
+  // single MMA issuer, not the softmax, bounds the unit period), so off by
+  // default; TTS_ROW_COPIES=2|4 enables them
+  static const int copies = std::getenv("TTS_ROW_COPIES") ? std::atoi(std::getenv("TTS_ROW_COPIES")) : 1;
+  p.copies = copies >= 4 ? 4 : copies >= 2 ? 2 : 1;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
   UInline inl;  // host staging of the parameter block (copied by the launch)
@@ -735,7 +863,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 1 : 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap3_k, c->tmap3_v, p, inl);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap_k, c->tmap3_v, p, inl);
   c->launches++;
   return e;
 }

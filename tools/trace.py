@@ -34,7 +34,16 @@ d = tr[1:n, 5] - tr[:n - 1, 5]
 print("median cycles per unit", np.median(d), "softmax busy median", np.median(tr[:n, 6] - tr[:n, 5]),
       "sfull wait median", np.median(tr[:n, 5] - tr[:n, 4]), "mma pfull-wait median", np.median(tr[:n, 2] - tr[:n, 1]))
 
-full = [j for j in range(n) if t2[j, 3] > 0]
+print("per-warp P arrive (rel. to warp 0) and MMA pfull_end (rel. to last warp), first 12 units:")
+for j in range(min(n, 12)):
+    a = t2[j, :4]
+    print(j, [int(x - a[0]) for x in a], "mma_pfull_end - last_arrive", int(tr[j, 2] - a.max()))
+print("median S-issue cycles (fullwait_end -> issue_s done):", np.median(tr[:n-1, 7] - tr[:n-1, 1]),
+      " issue_s done -> pfull_end:", np.median(tr[:n-1, 2] - tr[:n-1, 7]), " pfull_end -> pv_commit:", np.median(tr[:n-1, 3] - tr[:n-1, 2]),
+      " pv_commit -> next fullwait_start:", np.median(tr[1:n, 0] - tr[:n-1, 3]))
+d = t2[:n, :4] - t2[:n, :1]
+print("median arrive offsets vs warp 0:", np.median(d, axis=0), " median pfull_end - last arrive:", np.median(tr[:n, 2] - t2[:n, :4].max(1)))
+full = []
 print("member units", len(full), "of", n)
 if full:
     f = np.array(full)
