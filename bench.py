@@ -275,7 +275,11 @@ class SpanBench:
         self.cfg, self.world, self.rank = cfg, world, rank
         self.nl = cfg.N // world
         maxb = 2 * self.nl if world > 1 else cfg.N
-        pages = self.nl * workload.max_pages_per_beam(cfg) + 256  # every local lineage fully private
+        from paper_2509_00195_b200.runner import pages_per_request
+        if world == 1:
+            pages = pages_per_request(cfg) + 256  # the whole tree on one rank
+        else:
+            pages = self.nl * workload.max_pages_per_beam(cfg) + 256  # imported lineages are private copies
         self.tcfg = tts_config(cfg, 1, num_pages=pages, max_beams=maxb)
         self.ctx = Context(self.tcfg, dev_index)
         self.lib, self.h, self.dev = self.ctx.lib, self.ctx.h, self.ctx.device
