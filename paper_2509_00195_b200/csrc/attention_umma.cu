@@ -92,17 +92,13 @@ struct IntTag {
 };
 
 struct UParams {
-  int32_t* lens;              // device lengths: the appended beams' new length is stored
-  const int32_t* tables;
+  const int4* items;          // per-group distinct-page lists (k_plan), group slice at (req * maxB + beam0) * maxP
+  const int32_t* counts;      // items per group of the call (k_plan)
   const __nv_bfloat16* q;
   float* out;
   const GroupDesc* groups;    // device copies when the call does not fit the parameter block,
-  const int32_t* glens;       // else null (descriptors in UInline)
+                              // else null (descriptors in UInline)
   int32_t* status;
-  const uint4* k_new;         // null: no append (tts_prefix_attn_decode)
-  const uint4* v_new;
-  uint4* k_pool;
-  uint4* v_pool;
   int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits;
   int copies;                 // row copies R requested (1, 2, 4; reduced to what the group's rows allow)
   int64_t num_pages;
@@ -118,6 +114,138 @@ struct UInline {
 };
 
 // ---------------------------------------------------------------------------
+// a2 + a3 for one call, ahead of the attention kernel (which it releases early
+// through programmatic dependent launch).  Blocks [0, n_groups): the plan of
+// group gi -- its ordered list of DISTINCT pages (item = page, member-beam
+// mask, valid tokens, position; a run of adjacent beams holding the same page
+// id is one item), one thread per page position, written to the group's slice
+// of the items workspace, and the item count.  Blocks [n_groups, n_groups *
+// (1 + n_layers)) (only when appending): the call's new K/V row of each active
+// beam of one group for one layer and every kv head -> slot (len-1) % P of the
+// beam's last page (V -> the pool's fp16); a fresh page's slots 1..P-1 zeroed.
+struct PlanParams {
+  int32_t* lens;
+  const int32_t* tables;
+  const GroupDesc* groups;  // device copies when the call does not fit the parameter block, else null
+  const int32_t* glens;
+  int32_t* status;
+  const uint4* k_new;  // null: plan only (tts_prefix_attn_decode)
+  const uint4* v_new;
+  uint4* k_pool;
+  uint4* v_pool;
+  int4* items;
+  int32_t* counts;
+  int n_groups, layer_begin, n_call, Hkv, maxB, maxP;
+  int64_t num_pages;
+};
+constexpr int kPlanThreads = 512;
+
+__global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __grid_constant__ UInline inl) {
+  __shared__ int s_len[32];
+  __shared__ int s_wsum[kPlanThreads / 32];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (*(volatile int32_t*)p.status) return;
+  const bool plan = (int)blockIdx.x < p.n_groups;
+  const int gi = plan ? blockIdx.x : (blockIdx.x - p.n_groups) % p.n_groups;
+  const GroupDesc g = p.groups ? p.groups[gi] : inl.g[gi];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 32) {
+    const bool on = tid < g.nbeams && ((g.active >> tid) & 1u);
+    s_len[tid] = on ? (p.groups ? p.glens[g.pad[0] + tid] : inl.len[g.pad[0] + tid]) : 0;
+  }
+  __syncthreads();
+  const int nb = g.nbeams;
+  const int64_t row0 = (int64_t)g.req * p.maxB + g.beam0;
+  const int32_t* trow = p.tables + row0 * p.maxP;
+  if (!plan) {
+    const int lrel = (blockIdx.x - p.n_groups) / p.n_groups;
+    const int layer = p.layer_begin + lrel;
+    const int64_t plane = (int64_t)layer * p.num_pages * p.Hkv;
+    const int per_beam = p.Hkv * 16;
+    for (int w = tid; w < nb * per_beam; w += kPlanThreads) {
+      const int b = w / per_beam, rest = w % per_beam, kh = rest >> 4, e = rest & 15;
+      const int len = s_len[b];
+      if (len <= 0) continue;
+      const int pos = len - 1;
+      const int32_t page = trow[(int64_t)b * p.maxP + pos / kP];
+      const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + pos % kP) * 16 + e;
+      const int64_t src = ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + b) * p.Hkv + kh) * 16 + e;
+      p.k_pool[dst] = p.k_new[src];
+      p.v_pool[dst] = v_to_pool(p.v_new[src], p.status);
+    }
+    const int per_beam_z = p.Hkv * (kP - 1) * 16;
+    for (int w = tid; w < nb * per_beam_z; w += kPlanThreads) {
+      const int b = w / per_beam_z, rest = w % per_beam_z;
+      const int len = s_len[b];
+      if (len <= 0 || (len - 1) % kP != 0) continue;
+      const int kh = rest / ((kP - 1) * 16), r2 = rest % ((kP - 1) * 16);
+      const int32_t page = trow[(int64_t)b * p.maxP + (len - 1) / kP];
+      const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + 1 + r2 / 16) * 16 + (r2 & 15);
+      p.k_pool[dst] = make_uint4(0, 0, 0, 0);
+      p.v_pool[dst] = make_uint4(0, 0, 0, 0);
+    }
+    // generic-proxy stores -> the attention kernel's TMA (async proxy) reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    return;
+  }
+  if (p.k_new && tid < nb && s_len[tid] > 0) p.lens[row0 + tid] = s_len[tid];
+  const int npg = g.max_npages;
+  int4* out = p.items + row0 * p.maxP;
+  int base = 0;
+  for (int i0 = 0; i0 < npg; i0 += kPlanThreads) {
+    const int i = i0 + tid;
+    int t[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+      t[b] = (b < nb && i < npg && i * kP < s_len[b]) ? __ldg(trow + (int64_t)b * p.maxP + i) : -1;
+    int c = 0, last = -1;
+#pragma unroll
+    for (int b = 0; b < 32; ++b)
+      if (t[b] >= 0) {
+        c += t[b] != last;
+        last = t[b];
+      }
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kPlanThreads / 32; ++k) {
+      const int v = s_wsum[k];
+      wpre += k < wid ? v : 0;
+      tot += v;
+    }
+    int o = base + wpre + x - c;
+    last = -1;
+    int s0 = 0;
+    uint32_t mem = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      if (t[b] >= 0) {
+        if (t[b] != last) {
+          if (last >= 0) out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+          last = t[b];
+          mem = 1u << b;
+          s0 = b;
+        } else {
+          mem |= 1u << b;
+        }
+      }
+    }
+    if (last >= 0) out[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+    base += tot;
+    __syncthreads();
+  }
+  if (tid == 0) p.counts[gi] = base;
+}
+
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 2)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
@@ -131,26 +259,21 @@ __global__ void __launch_bounds__(kThreads, 2)
   float* m_s = reinterpret_cast<float*>(bp + kOffML);
   float* l_s = m_s + kRows;
   int4* scr = reinterpret_cast<int4*>(bp + kOffScr);
-  int* s_len = reinterpret_cast<int*>(bp + kOffLen);
+  int* s_bail = reinterpret_cast<int*>(bp + kOffLen);
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_append = b_qready + 8;
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
-  // programmatic dependent launch: everything this kernel reads may come from
-  // the previous kernel on the stream
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (*(volatile int32_t*)p.status) return;
-  asm volatile("griddepcontrol.launch_dependents;");
+  // Programmatic dependent launch: this grid starts while k_plan (the call's
+  // append + plan) runs.  The prologue below (barriers, TMEM, Q -> TMEM) reads
+  // nothing k_plan writes; the producer warp alone waits (griddepcontrol.wait)
+  // before it reads the plan, the pool or the status word.
   const int split = blockIdx.x % p.splits;
   const int gidx = blockIdx.x / p.splits;
   const GroupDesc g = p.groups ? p.groups[gidx] : inl.g[gidx];
   const int kh = blockIdx.y, lrel = blockIdx.z, layer = p.layer_begin + lrel;
   const int G = p.G;
-  if (threadIdx.x < 32) {
-    const bool on = threadIdx.x < g.nbeams && ((g.active >> threadIdx.x) & 1u);
-    s_len[threadIdx.x] = on ? (p.groups ? p.glens[g.pad[0] + threadIdx.x] : inl.len[g.pad[0] + threadIdx.x]) : 0;
-  }
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNS; ++i) {
@@ -163,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_init(b_pv + 8 * i, 1);
     }
     bar_init(b_qready, 4);
-    bar_init(b_append, 4);
+    *s_bail = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -220,81 +343,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) bar_arrive(b_qready);  // the MMA warp may start S = Q K^T
-    if (p.k_new) {
-      // a2: this (layer, kv head)'s new K/V row of every active beam -> slot
-      // (len-1) % P of its last page; a fresh page's slots 1..P-1 are zeroed so
-      // that masked columns never multiply stale (possibly non-finite) V
-      const int32_t* trow = p.tables + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
-      const int64_t plane = ((int64_t)layer * p.num_pages) * p.Hkv;
-      for (int w = threadIdx.x; w < g.nbeams * 16; w += 128) {
-        const int b = w >> 4, e = w & 15;
-        const int len = s_len[b];
-        if (len <= 0) continue;
-        const int pos = len - 1;
-        const int32_t page = trow[(int64_t)b * p.maxP + pos / kP];
-        const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + pos % kP) * 16 + e;
-        const int64_t src = ((((int64_t)layer * p.n_call + g.call_idx) * p.maxB + g.beam0 + b) * p.Hkv + kh) * 16 + e;
-        p.k_pool[dst] = p.k_new[src];
-        p.v_pool[dst] = v_to_pool(p.v_new[src], p.status);
-      }
-      for (int w = threadIdx.x; w < g.nbeams * (kP - 1) * 16; w += 128) {
-        const int b = w / ((kP - 1) * 16), rest = w % ((kP - 1) * 16);
-        const int len = s_len[b];
-        if (len <= 0 || (len - 1) % kP != 0) continue;
-        const int32_t page = trow[(int64_t)b * p.maxP + (len - 1) / kP];
-        const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + 1 + rest / 16) * 16 + (rest & 15);
-        p.k_pool[dst] = make_uint4(0, 0, 0, 0);
-        p.v_pool[dst] = make_uint4(0, 0, 0, 0);
-      }
-      // generic-proxy stores -> this CTA's TMA (async proxy) reads of the page
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      if (kh == 0 && lrel == 0 && split == 0 && threadIdx.x < g.nbeams && s_len[threadIdx.x] > 0)
-        p.lens[(int64_t)g.req * p.maxB + g.beam0 + threadIdx.x] = s_len[threadIdx.x];
-    }
-    __syncwarp();
-    if (lane == 0) bar_arrive(b_append);  // the producer may load the beams' last pages
   }
 
   if (threadIdx.x == 0) TTS_TR(1023, 1);  // prologue done (Q in TMEM)
 
   if (warp == 4) {
-    // ======================= producer: plan (a3) + TMA =======================
-    // Item = (page, member-beam mask, valid tokens, position), in position order
-    // and, within a position, in beam order: a run of adjacent beams (skipping
-    // beams that do not reach the position) holding the same page id is one
-    // item.  Units = consecutive item pairs; with a cluster split, this CTA
-    // takes units [u0, u1) of the group's list.
-    const int nb = g.nbeams, npg = g.max_npages;
-    const int32_t* trow = p.tables + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
-    int t[32];
-    auto load_col = [&](int i) {
-#pragma unroll
-      for (int b = 0; b < 32; ++b)
-        t[b] = (b < nb && i < npg && i * kP < s_len[b]) ? __ldg(trow + (int64_t)b * p.maxP + i) : -1;
-    };
-    auto count_runs = [&]() {
-      int c = 0, last = -1;
-#pragma unroll
-      for (int b = 0; b < 32; ++b)
-        if (t[b] >= 0) {
-          c += t[b] != last;
-          last = t[b];
-        }
-      return c;
-    };
-    int it_lo = 0, it_hi = 0x7fffffff;
-    if (p.splits > 1) {
-      int c = 0;
-      for (int i0 = 0; i0 < npg; i0 += 32) {
-        load_col(i0 + lane);
-        c += count_runs();
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      const int n_units = (c + kU - 1) / kU;
-      it_lo = (int)((int64_t)split * n_units / p.splits) * kU;
-      it_hi = min((int)((int64_t)(split + 1) * n_units / p.splits) * kU, c);
-    }
+    // ========================= producer: TMA =========================
+    // Units = consecutive pairs of the group's plan items (k_plan, a3); with a
+    // cluster split this CTA takes a contiguous, balanced range of them.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool bail = *(volatile int32_t*)p.status != 0;
+    const int nit = bail ? 0 : p.counts[gidx];
+    const int n_units = (nit + 1) / 2;
+    const int u_lo = (int)((int64_t)split * n_units / p.splits);
+    const int u_hi = (int)((int64_t)(split + 1) * n_units / p.splits);
+    const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
     const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
     int slot = 0;
     uint32_t ph = 0;
@@ -322,69 +385,30 @@ __global__ void __launch_bounds__(kThreads, 2)
         ph ^= 1u;
       }
     };
-    // the first position holding a page this CTA appended to: TMA of it (and
-    // of everything after it) waits for the append stores of warps 0-3
-    int p_min = 0x7fffffff;
-    if (p.k_new)
-      for (int b = 0; b < nb; ++b)
-        if (s_len[b] > 0) p_min = min(p_min, (s_len[b] - 1) / kP);
-    bool app_wait = p_min != 0x7fffffff;
-    int4 pend = make_int4(-2, 0, 0, 0);
-    bool has_pend = false;
-    int done = 0;  // items of earlier batches
-    // W positions per batch (lane < W), W * nb <= kScrItems
-    const int W = nb <= 16 ? 32 : 16;
-    if (npg > 0) load_col(lane < W ? lane : npg);
-    for (int i0 = 0; i0 < npg && done < it_hi; i0 += W) {
-      const int i = lane < W ? i0 + lane : npg;
-      const int c = count_runs();
-      int x = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+    // 32 units per batch (lane = unit); the next batch's loads are in flight
+    // while lane 0 issues the current one
+    int4 a0 = make_int4(-2, 0, 0, 0), a1 = a0;
+    auto load = [&](int u0) {
+      const int u = u0 + lane;
+      if (u < u_hi) {
+        a0 = its[2 * u];
+        a1 = 2 * u + 1 < nit ? its[2 * u + 1] : make_int4(-2, 0, 0, 0);
       }
-      const int tot = __shfl_sync(0xffffffffu, x, 31);
-      int o = x - c;
-      int last = -1, s0 = 0;
-      uint32_t mem = 0;
-#pragma unroll
-      for (int b = 0; b < 32; ++b) {
-        if (t[b] >= 0) {
-          if (t[b] != last) {
-            if (last >= 0) scr[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
-            last = t[b];
-            mem = 1u << b;
-            s0 = b;
-          } else {
-            mem |= 1u << b;
-          }
-        }
-      }
-      if (last >= 0) scr[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+    };
+    load(u_lo);
+    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
+      scr[2 * lane] = a0;
+      scr[2 * lane + 1] = a1;
       __syncwarp();
-      if (i0 + W < npg) load_col(lane < W ? i + W : npg);  // next batch's loads in flight while lane 0 issues
+      if (u0 + 32 < u_hi) load(u0 + 32);
       if (lane == 0) {
-        for (int k = max(0, it_lo - done); k < tot && done + k < it_hi; ++k) {
-          const int4 m = scr[k];
-          if (app_wait && m.w >= p_min) {
-            bar_wait(b_append, 0);
-            app_wait = false;
-          }
-          if (has_pend) {
-            issue(pend, m);
-            has_pend = false;
-          } else {
-            pend = m;
-            has_pend = true;
-          }
-        }
+        const int n = min(32, u_hi - u0);
+        for (int k = 0; k < n; ++k) issue(scr[2 * k], scr[2 * k + 1]);
       }
-      done += tot;
       __syncwarp();
     }
     if (lane == 0) {
-      if (has_pend) issue(pend, make_int4(-2, 0, 0, 0));
+      if (bail) *s_bail = 1;
       bar_wait(b_empty + 8 * slot, ph ^ 1u);
       meta[slot * kU] = make_int4(-1, 0, 0, 0);
       bar_arrive(b_full + 8 * slot);
@@ -724,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int cseg = threadIdx.x % tpr;
       const int cw = kD / tpr;
       const int bl = row / G;
-      const bool ok = row < nrows && ((g.active >> bl) & 1u);
+      const bool ok = row < nrows && ((g.active >> bl) & 1u) && !*s_bail;
       const uint32_t lm = su32(m_s + row), ll = su32(l_s + row);
       // all remote loads of a step are issued before any is consumed (DSMEM
       // latency ~200 cycles; dependent loads would serialise)
@@ -798,18 +822,33 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
                                   int n_lens, int splits, int layer_begin, int n_layers, int n_call,
                                   const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
                                   const __nv_bfloat16* v_new, cudaStream_t st) {
+  PlanParams pp;
+  pp.lens = c->buf.seq_lens;
+  pp.tables = c->buf.block_tables;
+  pp.groups = nullptr;
+  pp.glens = nullptr;
+  pp.status = c->buf.status;
+  pp.k_new = (const uint4*)k_new;
+  pp.v_new = (const uint4*)v_new;
+  pp.k_pool = (uint4*)c->buf.k_pool;
+  pp.v_pool = (uint4*)c->buf.v_pool;
+  pp.items = c->ws_items;
+  pp.counts = c->ws_counts;
+  pp.n_groups = n_groups;
+  pp.layer_begin = layer_begin;
+  pp.n_call = n_call;
+  pp.Hkv = c->cfg.num_kv_heads;
+  pp.maxB = c->cfg.max_beams;
+  pp.maxP = c->cfg.max_pages_per_beam;
+  pp.num_pages = c->cfg.num_pages;
+
   UParams p;
-  p.lens = c->buf.seq_lens;
-  p.tables = c->buf.block_tables;
+  p.items = c->ws_items;
+  p.counts = c->ws_counts;
   p.q = q;
   p.out = out;
   p.groups = nullptr;
-  p.glens = nullptr;
   p.status = c->buf.status;
-  p.k_new = (const uint4*)k_new;
-  p.v_new = (const uint4*)v_new;
-  p.k_pool = (uint4*)c->buf.k_pool;
-  p.v_pool = (uint4*)c->buf.v_pool;
   p.layer_begin = layer_begin;
   p.n_call = n_call;
   p.Hq = c->cfg.num_q_heads;
@@ -835,7 +874,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     upload2(c, groups_h, (size_t)n_groups * sizeof(GroupDesc), lens_h, (size_t)n_lens * 4, st, &e, &dg, &dl);
     if (e != cudaSuccess) return e;
     p.groups = (const GroupDesc*)dg;
-    p.glens = (const int32_t*)dl;
+    pp.groups = (const GroupDesc*)dg;
+    pp.glens = (const int32_t*)dl;
   }
   static bool attr_done = false;
   if (!attr_done) {
@@ -845,6 +885,23 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     e = cudaFuncSetAttribute(k_tree_umma, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr_done = true;
+  }
+  static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
+  cudaLaunchAttribute pdl;
+  // each kernel may start while its predecessor on the stream runs; both wait
+  // (griddepcontrol.wait) before touching what the predecessor writes
+  pdl.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl.val.programmaticStreamSerializationAllowed = 1;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_groups * (k_new ? 1 + n_layers : 1));
+    cfg.blockDim = dim3(kPlanThreads);
+    cfg.stream = st;
+    cfg.attrs = &pdl;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_plan, pp, inl);
+    c->launches++;
+    if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_groups * splits, p.Hkv, n_layers);
@@ -856,11 +913,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   attr[0].val.clusterDim.x = splits;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  // the prologue of this launch may overlap the tail of the previous kernel;
-  // the kernel waits (griddepcontrol.wait) before touching global memory
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
+  attr[1] = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 1 : 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap_k, c->tmap3_v, p, inl);
