@@ -186,9 +186,12 @@ class Bench:
             from paper_2509_00195_b200.tts import TTSError
             raise TTSError(code, what)
 
-    def run_step(self, stats_accum=None, e2e=None):
-        """One full run of every request.  e2e: dict of pinned host rings to copy from."""
+    def run_step(self, stats_accum=None, e2e=None, seg=None):
+        """One full run of every request.  e2e: dict of pinned host rings to copy from.
+        seg: list receiving one CUDA event pair (on the launching stream) per run of
+        consecutive decode calls between two forks (install / release excluded)."""
         c = self.cfg
+        open_ev = None
         lib, h, st = self.lib, self.h, self.stream
         for r in self.greqs:
             k, v = self.prompt[self.local[r]]
@@ -201,6 +204,9 @@ class Bench:
         decode = lib.tts_decode_step
         for it in self.sched:
             q, k, v = self.ring[it.t % nr]
+            if seg is not None and open_ev is None:
+                open_ev = torch.cuda.Event(enable_timing=True)
+                open_ev.record(torch.cuda.current_stream(self.dev))
             if e2e is None and not self.batched and stats_accum is None:
                 # hot loop: one C-ABI call per request and position, arguments pre-marshalled
                 qp, kp, vp = ptrs[it.t % nr]
@@ -241,6 +247,12 @@ class Bench:
                             self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum[self.ncall].data_ptr(),
                                                                 st), "stats")
                             self.ncall += 1
+            if it.forks or (seg is not None and it is self.sched[-1]):
+                if seg is not None:
+                    e_end = torch.cuda.Event(enable_timing=True)
+                    e_end.record(torch.cuda.current_stream(self.dev))
+                    seg.append((open_ev, e_end))
+                    open_ev = None
             if it.forks:
                 loc = [self.local[r] for r, _ in it.forks]
                 arr = (ctypes.c_int32 * len(loc))(*loc)
@@ -311,14 +323,18 @@ class SpanBench:
             from paper_2509_00195_b200.tts import TTSError
             raise TTSError(code, what)
 
-    def run_step(self, stats_accum=None, e2e=None):
+    def run_step(self, stats_accum=None, e2e=None, seg=None):
         from paper_2509_00195_b200.dist import select_fork_global
         c, lib, h, st = self.cfg, self.lib, self.h, self.stream
         k, v = self.prompt
         self._chk(lib.tts_block_table_init_request(h, 0, self.nl, c.prompt, k.data_ptr(), v.data_ptr(), st), "init")
         nr = len(self.ring)
+        open_ev = None
         for it in self.sched:
             q, k, v = self.ring[it.t % nr]
+            if seg is not None and open_ev is None:
+                open_ev = torch.cuda.Event(enable_timing=True)
+                open_ev.record(torch.cuda.current_stream(self.dev))
             if e2e is not None:
                 hq, hk, hv = e2e["ring"][it.t % nr]
                 q, k, v = e2e["q"], e2e["k"], e2e["v"]
@@ -331,6 +347,11 @@ class SpanBench:
                 self._chk(lib.tts_block_table_stats(h, 1, self.req, None, stats_accum[self.ncall].data_ptr(), st),
                           "stats")
                 self.ncall += 1
+            if seg is not None and (it.forks or it is self.sched[-1]):
+                e_end = torch.cuda.Event(enable_timing=True)
+                e_end.record(torch.cuda.current_stream(self.dev))
+                seg.append((open_ev, e_end))
+                open_ev = None
             for (_, s) in it.forks:
                 sc = self.scores[s]
                 if e2e is not None:
@@ -489,25 +510,26 @@ def main():
     clk = clocks.stop()
     assert b.ctx.tts_device_status() == 0, "device status error in timed region"
 
-    # kernel-duration pass: the same K steps again, a CUDA event pair on the
-    # launching stream around every attention launch (tts_profile_*).  Kept out
-    # of the headline region: an event record between two launches costs the
-    # step ~7 us (it serialises the programmatic-dependent-launch overlap) and
-    # inflates each measured launch by its launch latency, so the kernel
-    # duration (and the roofline fraction) measured here is conservative.
-    b.ctx.tts_profile_begin()
+    # kernel-duration pass: the same K steps again, with a CUDA event pair on the
+    # launching stream around every run of decode calls between two forks (the
+    # decode-step kernels: k_plan + k_tree_umma per call, k_alloc on page
+    # crossings).  Events between individual calls would serialise the
+    # programmatic-dependent-launch overlap of consecutive calls, so they are
+    # only placed where a fork breaks the chain anyway.
+    segs = []
     barrier(ws)
     torch.cuda.synchronize(dev)
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(st)
     for _ in range(args.steps):
-        b.run_step()
+        b.run_step(seg=segs)
     p1.record(st)
     torch.cuda.synchronize(dev)
     barrier(ws)
     ms_prof = p0.elapsed_time(p1)
-    attn_ms, attn_launches = b.ctx.tts_profile_end()
+    attn_ms = sum(a.elapsed_time(z) for a, z in segs)
+    attn_launches = b.n_calls * args.steps
     assert b.ctx.tts_device_status() == 0, "device status error in profiled pass"
 
     ms_max = allmax(ms, ws, dev)
@@ -578,16 +600,17 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk, "unit": "GB/s",
                          "frac": achieved_gbs / pk, "traffic": traffic, "traffic_over_algo": traffic_ratio,
                          "peak_source": pk_src,
-                         "kernel": "k_tree_umma (one launch per call: a2 append + a3 plan + a4 tcgen05 prefix-shared attention)",
+                         "kernel": "decode step: k_plan (a2 append + a3 plan) + k_tree_umma (a4/a5 tcgen05 "
+                                   "prefix-shared attention), PDL-chained; + k_alloc on page crossings",
                          "algo_bytes": "unique KV (valid tokens of distinct pages) + q bf16 + out fp32",
                          "unique_kv_gbs": unique_gbs, "logical_kv_gbs": logical_gbs,
                          "reuse": logical_tok / max(unique_tok, 1),
                          "attn_ms_per_step": attn_ms / args.steps, "attn_launches_per_step": attn_launches // args.steps,
                          "attn_us_per_launch": attn_ms * 1e3 / max(attn_launches, 1),
                          "attn_share_of_step": attn_ms / ms_prof,
-                         "timing": "separate K-step pass with a CUDA event pair per launch on the launching "
-                                   f"stream ({ms_prof / args.steps:.1f} ms/step with events vs "
-                                   f"{ms / args.steps:.1f} clean)"},
+                         "timing": "separate K-step pass, a CUDA event pair on the launching stream around every "
+                                   f"run of decode calls between forks ({len(segs)} pairs; "
+                                   f"{ms_prof / args.steps:.1f} ms/step with events vs {ms / args.steps:.1f} clean)"},
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),

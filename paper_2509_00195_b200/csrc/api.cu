@@ -25,8 +25,8 @@ size_t workspace_bytes(const tts_config_t& c) {
   s += align_up((size_t)max_alloc_items(c) * 4);   // page list
   s += align_up((size_t)max_alloc_items(c) * sizeof(CowCopy));
   s += align_up((size_t)c.num_pages * 4);           // stats marks
-  s += align_up(rows * c.max_pages_per_beam * 16);  // attention plan items
-  s += align_up(rows * 4);                          // plan counts
+  s += align_up(2 * rows * c.max_pages_per_beam * 16);  // attention plan items (double-buffered)
+  s += align_up(2 * rows * 4);                          // plan counts
   s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
   return s;
 }
@@ -157,9 +157,9 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   c->ws_mark = (int32_t*)w;
   w += tts::align_up((size_t)cfg->num_pages * 4);
   c->ws_items = (int4*)w;
-  w += tts::align_up(rws * cfg->max_pages_per_beam * 16);
+  w += tts::align_up(2 * rws * cfg->max_pages_per_beam * 16);
   c->ws_counts = (int32_t*)w;
-  w += tts::align_up(rws * 4);
+  w += tts::align_up(2 * rws * 4);
   c->ws_upload = w;
   if (cudaMallocHost(&c->pinned, (size_t)tts::kUploadSlots * tts::kUploadSlotBytes) != cudaSuccess) {
     delete c;

@@ -48,7 +48,7 @@ constexpr int kNS = 6;                       // ring slots (units)
 constexpr int kTile = kP * kD * 2;           // 4 KiB: one (page, kv head) K or V tile
 constexpr int kSlot = 2 * kU * kTile;        // 16 KiB: K tiles then V tiles
 constexpr int kRing = kNS * kSlot;           // 64 KiB
-constexpr int kThreads = 192;                // warps 0-3 softmax, 4 producer, 5 MMA
+constexpr int kThreads = 224;                // warps 0-3 softmax, 4 producer, 5 S issuer, 6 PV issuer
 constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
 constexpr int kSCols = kU * kP;              // 32
 
@@ -67,6 +67,17 @@ static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
 #ifdef TTS_TRACE
 __device__ long long g_trace[1024][8];
 __device__ long long g_trace2[1024][8];
+__device__ long long g_cta[4096][4];  // per CTA of the last launch: globaltimer at start / loop end / exit, units | smid << 32
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TTS_CTA(ev, v)                                                                          \
+  do {                                                                                          \
+    const int id_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
+    if (id_ < 4096) g_cta[id_][(ev)] = (v);                                                    \
+  } while (0)
 #define TTS_TR(j, ev)                                                                   \
   do {                                                                                  \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
@@ -78,6 +89,9 @@ __device__ long long g_trace2[1024][8];
       g_trace2[(j)][(ev)] = clock64();                                                  \
   } while (0)
 #else
+#define TTS_CTA(ev, v) \
+  do {                 \
+  } while (0)
 #define TTS_TR(j, ev) \
   do {                \
   } while (0)
@@ -85,11 +99,6 @@ __device__ long long g_trace2[1024][8];
   do {                 \
   } while (0)
 #endif
-
-template <int N>
-struct IntTag {
-  static constexpr int value = N;
-};
 
 struct UParams {
   const int4* items;          // per-group distinct-page lists (k_plan), group slice at (req * maxB + beam0) * maxP
@@ -100,7 +109,6 @@ struct UParams {
                               // else null (descriptors in UInline)
   int32_t* status;
   int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits;
-  int copies;                 // row copies R requested (1, 2, 4; reduced to what the group's rows allow)
   int64_t num_pages;
   float scale_log2;
 };
@@ -138,14 +146,24 @@ struct PlanParams {
   int n_groups, layer_begin, n_call, Hkv, maxB, maxP;
   int64_t num_pages;
 };
-constexpr int kPlanThreads = 512;
+constexpr int kPlanThreads = 128;  // small enough to co-reside with two attention CTAs per SM
 
-__global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __grid_constant__ UInline inl) {
+__global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __grid_constant__ UInline inl) {
   __shared__ int s_len[32];
   __shared__ int s_wsum[kPlanThreads / 32];
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (*(volatile int32_t*)p.status) return;
+  // Programmatic dependent launch: this grid may run while the previous call's
+  // attention kernel still streams its pages.  Nothing here conflicts with it:
+  // the plan goes to the other half of the double-buffered items workspace,
+  // the new token lands in a slot the previous call masks (its P is exactly 0
+  // and the pool never holds a non-finite V), and a fresh page (zero fill) only
+  // exists after a k_alloc launch, which is ordered after the previous call.
+  // The grid completes only after the previous kernel has (griddepcontrol.wait
+  // at the end), so the attention kernel that waits on this grid also waits on
+  // every earlier call.
+  if (*(volatile int32_t*)p.status) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   const bool plan = (int)blockIdx.x < p.n_groups;
   const int gi = plan ? blockIdx.x : (blockIdx.x - p.n_groups) % p.n_groups;
   const GroupDesc g = p.groups ? p.groups[gi] : inl.g[gi];
@@ -159,34 +177,58 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __gri
   const int64_t row0 = (int64_t)g.req * p.maxB + g.beam0;
   const int32_t* trow = p.tables + row0 * p.maxP;
   if (!plan) {
+    // the beams' last pages first, so that the copy loop below has only
+    // independent loads (4 in flight per thread)
+    __shared__ int s_page[32];
+    if (tid < 32) s_page[tid] = (tid < nb && s_len[tid] > 0) ? trow[(int64_t)tid * p.maxP + (s_len[tid] - 1) / kP] : -1;
+    __syncthreads();
     const int lrel = (blockIdx.x - p.n_groups) / p.n_groups;
     const int layer = p.layer_begin + lrel;
     const int64_t plane = (int64_t)layer * p.num_pages * p.Hkv;
     const int per_beam = p.Hkv * 16;
-    for (int w = tid; w < nb * per_beam; w += kPlanThreads) {
-      const int b = w / per_beam, rest = w % per_beam, kh = rest >> 4, e = rest & 15;
-      const int len = s_len[b];
-      if (len <= 0) continue;
-      const int pos = len - 1;
-      const int32_t page = trow[(int64_t)b * p.maxP + pos / kP];
-      const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + pos % kP) * 16 + e;
-      const int64_t src = ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + b) * p.Hkv + kh) * 16 + e;
-      p.k_pool[dst] = p.k_new[src];
-      p.v_pool[dst] = v_to_pool(p.v_new[src], p.status);
+    const uint4* __restrict__ kn = p.k_new;
+    const uint4* __restrict__ vn = p.v_new;
+    constexpr int kBatch = 4;
+    for (int w0 = tid; w0 < nb * per_beam; w0 += kBatch * kPlanThreads) {
+      uint4 kv[kBatch], vv[kBatch];
+      int64_t dst[kBatch];
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int w = w0 + i * kPlanThreads;
+        dst[i] = -1;
+        if (w < nb * per_beam) {
+          const int b = w / per_beam, rest = w % per_beam, kh = rest >> 4, e = rest & 15;
+          const int page = s_page[b];
+          if (page >= 0) {
+            const int pos = s_len[b] - 1;
+            dst[i] = ((plane + (int64_t)page * p.Hkv + kh) * kP + pos % kP) * 16 + e;
+            const int64_t src = ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + b) * p.Hkv + kh) * 16 + e;
+            kv[i] = __ldg(kn + src);
+            vv[i] = __ldg(vn + src);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i)
+        if (dst[i] >= 0) {
+          p.k_pool[dst[i]] = kv[i];
+          p.v_pool[dst[i]] = v_to_pool(vv[i], p.status);
+        }
     }
-    const int per_beam_z = p.Hkv * (kP - 1) * 16;
-    for (int w = tid; w < nb * per_beam_z; w += kPlanThreads) {
-      const int b = w / per_beam_z, rest = w % per_beam_z;
-      const int len = s_len[b];
-      if (len <= 0 || (len - 1) % kP != 0) continue;
-      const int kh = rest / ((kP - 1) * 16), r2 = rest % ((kP - 1) * 16);
-      const int32_t page = trow[(int64_t)b * p.maxP + (len - 1) / kP];
-      const int64_t dst = ((plane + (int64_t)page * p.Hkv + kh) * kP + 1 + r2 / 16) * 16 + (r2 & 15);
-      p.k_pool[dst] = make_uint4(0, 0, 0, 0);
-      p.v_pool[dst] = make_uint4(0, 0, 0, 0);
+    // a fresh page (first token at slot 0): zero its slots 1..P-1 (a beam-uniform test)
+    for (int b = 0; b < nb; ++b) {
+      if (s_page[b] < 0 || (s_len[b] - 1) % kP != 0) continue;
+      for (int w = tid; w < p.Hkv * (kP - 1) * 16; w += kPlanThreads) {
+        const int kh = w / ((kP - 1) * 16), r2 = w % ((kP - 1) * 16);
+        const int64_t dst = ((plane + (int64_t)s_page[b] * p.Hkv + kh) * kP + 1 + r2 / 16) * 16 + (r2 & 15);
+        p.k_pool[dst] = make_uint4(0, 0, 0, 0);
+        p.v_pool[dst] = make_uint4(0, 0, 0, 0);
+      }
     }
     // generic-proxy stores -> the attention kernel's TMA (async proxy) reads
     asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    asm volatile("griddepcontrol.launch_dependents;");
     return;
   }
   if (p.k_new && tid < nb && s_len[tid] > 0) p.lens[row0 + tid] = s_len[tid];
@@ -195,17 +237,18 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __gri
   int base = 0;
   for (int i0 = 0; i0 < npg; i0 += kPlanThreads) {
     const int i = i0 + tid;
-    int t[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      t[b] = (b < nb && i < npg && i * kP < s_len[b]) ? __ldg(trow + (int64_t)b * p.maxP + i) : -1;
+    // entry of beam b at position i (-1: the beam does not reach it); read
+    // twice (count, then write) instead of held in registers
+    auto entry = [&](int b) { return (i < npg && i * kP < s_len[b]) ? __ldg(trow + (int64_t)b * p.maxP + i) : -1; };
     int c = 0, last = -1;
-#pragma unroll
-    for (int b = 0; b < 32; ++b)
-      if (t[b] >= 0) {
-        c += t[b] != last;
-        last = t[b];
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) {
+      const int t = entry(b);
+      if (t >= 0) {
+        c += t != last;
+        last = t;
       }
+    }
     int x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -225,12 +268,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __gri
     last = -1;
     int s0 = 0;
     uint32_t mem = 0;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) {
-      if (t[b] >= 0) {
-        if (t[b] != last) {
+#pragma unroll 8
+    for (int b = 0; b < nb; ++b) {
+      const int t = entry(b);
+      if (t >= 0) {
+        if (t != last) {
           if (last >= 0) out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
-          last = t[b];
+          last = t;
           mem = 1u << b;
           s0 = b;
         } else {
@@ -243,9 +287,15 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(PlanParams p, const __gri
     __syncthreads();
   }
   if (tid == 0) p.counts[gi] = base;
+  __threadfence();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (blockIdx.x == 0 && tid == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
+// kPoly: every other pair of exponentials on the FMA/ALU pipes (ex2_poly2)
+// instead of MUFU, halving the softmax warps' MUFU occupancy
+template <bool kPoly>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
@@ -265,6 +315,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
+  if (threadIdx.x == 0) TTS_CTA(0, gtimer());
+  // the next call's k_plan may start as soon as every CTA of this grid runs
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   // Programmatic dependent launch: this grid starts while k_plan (the call's
   // append + plan) runs.  The prologue below (barriers, TMEM, Q -> TMEM) reads
   // nothing k_plan writes; the producer warp alone waits (griddepcontrol.wait)
@@ -294,26 +347,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // Rows of the tile.  The group's nrows = nbeams x G query rows are placed
-  // R = 128 / RS times (RS = 32, 64 or 128 lanes per copy, the smallest that
-  // holds them): copy `rep` (lanes [rep*RS, (rep+1)*RS)) owns columns
-  // [rep*32/R, (rep+1)*32/R) of every 32-column unit, so a small group's
-  // softmax work is spread over all four lane quadrants (warps) instead of
-  // one; the R partial states of a row are merged in the epilogue like a
-  // split-KV merge.  Row br of a copy -> (beam g.beam0 + br / G, q head kh*G + br % G).
-  const int nrows = g.nbeams * G;
-  int R = p.copies;
-  while (R > 1 && nrows > kRows / R) R >>= 1;
-  const int RS = kRows / R;
+  // Rows of the tile, balanced over the four lane quadrants (softmax warps):
+  // warp w holds beams [w*bpw, (w+1)*bpw) of the group, G consecutive lanes
+  // per beam (host: bpw * G <= 32).  A page's exponentials are computed only by
+  // the warps holding one of its member beams, so spreading the beams evenly
+  // spreads the softmax work of private pages over all four warps.
+  const int bpw = (g.nbeams + 3) >> 2;
+  auto row_of = [&](int row, int& beam, int& head) {
+    const int l = row & 31, bw = l / G;
+    beam = (row >> 5) * bpw + bw;
+    head = l - bw * G;
+    return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
+  };
   const int r = threadIdx.x;
-  const int rep = r / RS, br = r % RS;
-  const int rbl = br / G;
-  const bool rvalid = warp < 4 && br < nrows && ((g.active >> rbl) & 1u);
+  int rbl = 0, rh = 0;
+  const bool rvalid = warp < 4 && row_of(r, rbl, rh);
   uint32_t qv[64];  // this thread's query row (bf16 pairs), loaded before the TMEM handshake
   if (warp < 4) {
     const uint4* src = reinterpret_cast<const uint4*>(
         p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (rvalid ? rbl : 0)) * p.Hq + kh * G +
-               (rvalid ? br % G : 0)) * kD);
+               (rvalid ? rh : 0)) * kD);
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const uint4 v = rvalid ? src[c] : make_uint4(0, 0, 0, 0);
@@ -355,6 +408,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool bail = *(volatile int32_t*)p.status != 0;
     const int nit = bail ? 0 : p.counts[gidx];
     const int n_units = (nit + 1) / 2;
+#ifdef TTS_TRACE
+    if (lane == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      TTS_CTA(3, (long long)n_units | ((long long)smid << 32));
+    }
+#endif
     const int u_lo = (int)((int64_t)split * n_units / p.splits);
     const int u_hi = (int)((int64_t)(split + 1) * n_units / p.splits);
     const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
@@ -414,56 +474,51 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_arrive(b_full + 8 * slot);
     }
   } else if (warp == 5) {
-    // ============================ MMA issuer ============================
+    // ========================= S issuer: S = Q K^T =========================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
-    // elected lane issues the tcgen05 instructions.
+    // elected lane issues.  S and PV are issued by two warps so that neither
+    // waits behind the other's issue (the tensor pipe runs both in issue order).
     constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
-    constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
-    const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);    // K tiles: K-major SW128
-    const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
-    auto issue_s = [&](int j) {
+    const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);  // K tiles: K-major SW128
+    bar_wait(b_qready, 0);  // Q in TMEM
+    for (int j = 0;; ++j) {
+      const int slot = j % kNS;
+      if (lane == 0) TTS_TR(j, 0);
+      bar_wait(b_full + 8 * slot, (j / kNS) & 1u);
+      if (lane == 0) TTS_TR(j, 1);
+      tc_fence_after();
+      if (meta[slot * kU].x == -1) {
+        if (elect_one()) bar_arrive(b_sfull + 8 * (j & 1));  // the softmax warps see the sentinel
+        __syncwarp();
+        break;
+      }
+      // S buffer j & 1 holds P(j - 2) until PV(j - 2) has read it
+      if (j >= 2) bar_wait(b_pv + 8 * (j & 1), ((j - 2) >> 1) & 1u);
+      tc_fence_after();
       // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
       // absent second page leaves columns 16..31 undefined; they are masked)
-      const int slot = j % kNS;
       const uint32_t sd = t_s + (j & 1) * kSCols;
       const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < kD / 16; ++ks)
-          mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s,
-                 ks > 0);
+          mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s, ks > 0);
         tc_commit(b_sfull + 8 * (j & 1));
       }
       __syncwarp();
-    };
-    bar_wait(b_qready, 0);  // Q in TMEM
-    bar_wait(b_full, 0);
-    tc_fence_after();
-    bool done = meta[0].x == -1;
-    if (done) {
-      if (elect_one()) bar_arrive(b_sfull);
-      __syncwarp();
-    } else {
-      issue_s(0);
+      if (lane == 0) TTS_TR(j, 7);
     }
+  } else if (warp == 6) {
+    // ====================== PV issuer: O += P V ======================
+    constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
+    const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
     uint32_t acc = 0;
-    for (int j = 0; !done; ++j) {
-      const int sn = (j + 1) % kNS;
-      if (lane == 0) TTS_TR(j, 0);
-      bar_wait(b_full + 8 * sn, ((j + 1) / kNS) & 1u);
-      if (lane == 0) TTS_TR(j, 1);
-      tc_fence_after();
-      const bool last = meta[sn * kU].x == -1;
-      if (last) {
-        if (elect_one()) bar_arrive(b_sfull + 8 * ((j + 1) & 1));
-        __syncwarp();
-      } else {
-        issue_s(j + 1);
-        if (lane == 0) TTS_TR(j, 7);
-      }
+    for (int j = 0;; ++j) {
+      const int slot = j % kNS;
+      bar_wait(b_full + 8 * slot, (j / kNS) & 1u);
+      if (meta[slot * kU].x == -1) break;
       bar_wait(b_pfull + 8 * (j & 1), (j >> 1) & 1u);
       if (lane == 0) TTS_TR(j, 2);
-      const int slot = j % kNS;
       tc_fence_after();
       const uint32_t pa = t_s + (j & 1) * kSCols;
       const bool e = elect_one();
@@ -471,161 +526,148 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int k = 0; k < kU; ++k) {
         if (meta[slot * kU + k].x < 0) continue;
         const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
-        if (e) {
-          mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
-        }
+        if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
         acc = 1;
       }
       if (e) {
+        // S(j) completed before the softmax produced P(j), so this commit
+        // covers every read of the slot
         tc_commit(b_empty + 8 * slot);
         tc_commit(b_pv + 8 * (j & 1));
         TTS_TR(j, 3);
       }
       __syncwarp();
-      done = last;
     }
-  } else {
+  } else if (warp < 4) {
     // ============================ softmax (warps 0-3) ============================
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     float m_ref = -1e30f, l = 0.f;
     int j = 0;
-    auto loop = [&](auto cw_tag) {
-      constexpr int CW = decltype(cw_tag)::value;  // columns of every unit this copy owns
-      constexpr int PW = CW < kP ? CW : kP;        // of which per page
-      constexpr int NPG = CW / PW;                 // pages they touch (2 or 1)
-      const int c0 = rep * CW;                     // first owned column of the unit
-      const int kk0 = c0 / kP, t0 = c0 % kP;       // its page and token slot
-      for (;; ++j) {
-        if (r == 0) TTS_TR(j, 4);
-        bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
-        if (r == 0) TTS_TR(j, 5);
-        tc_fence_after();
-        const int slot = j % kNS;
-        if (meta[slot * kU].x == -1) break;
-        int4 mt[NPG];
-        bool mem[NPG], wm[NPG];
-        bool wany = false;
+    for (;; ++j) {
+      if (r == 0) TTS_TR(j, 4);
+      bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
+      if (r == 0) TTS_TR(j, 5);
+      tc_fence_after();
+      const int slot = j % kNS;
+      if (meta[slot * kU].x == -1) break;
+      int4 mt[kU];
+      bool mem[kU], wm[kU];
+      bool wany = false;
 #pragma unroll
-        for (int k = 0; k < NPG; ++k) {
-          mt[k] = meta[slot * kU + kk0 + k];
-          // warp-uniform page membership: a warp none of whose rows reads a
-          // page skips its exponentials (P = 0 there)
-          mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
-          wm[k] = __any_sync(0xffffffffu, mem[k]);
-          wany |= wm[k];
-        }
-        uint32_t pk[CW / 2];
+      for (int k = 0; k < kU; ++k) {
+        mt[k] = meta[slot * kU + k];
+        // warp-uniform page membership: a warp none of whose rows reads a
+        // page skips its exponentials (P = 0 there)
+        mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
+        wm[k] = __any_sync(0xffffffffu, mem[k]);
+        wany |= wm[k];
+      }
+      uint32_t pk[kSCols / 2];
 #pragma unroll
-        for (int i = 0; i < CW / 2; ++i) pk[i] = 0u;
-        if (wany) {
-          float v[CW];
-          {
-            uint32_t sr[CW];
-            const uint32_t ta = t_s + lane_off + (j & 1) * kSCols + c0;
-            if constexpr (CW == 32) {
-              tc_ld32(ta, sr);
-            } else if constexpr (CW == 16) {
-              tc_ld16(ta, sr);
-            } else {
-              tc_ld8(ta, sr);
-            }
+      for (int i = 0; i < kSCols / 2; ++i) pk[i] = 0u;
+      if (wany) {
+        float v[kSCols];
+        {
+          // only the pages this warp's rows read: TMEM read bandwidth is a
+          // shared per-SM resource (a private page is read by one warp)
+          uint32_t sr[kSCols];
+#ifdef TTS_LD32
+          tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
+#else
+          if (wm[0] && wm[1]) {
+            tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
             tc_wait_ld();
 #pragma unroll
-            for (int i = 0; i < CW; ++i) v[i] = __uint_as_float(sr[i]);
-          }
-          // raw scores (scale > 0 commutes with max); rows not reading page k
-          // are masked once per page (max -> -inf, exponent offset -> -inf, so
-          // P is exactly 0); token slots >= ntok only on a partial page
-          float mx = -INFINITY;
+            for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
+          } else {
+            // one page: 16 columns
+            const int k1 = wm[0] ? 0 : 1;
+            tc_ld16(t_s + lane_off + (j & 1) * kSCols + k1 * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
+            tc_wait_ld();
 #pragma unroll
-          for (int k = 0; k < NPG; ++k) {
-            if (mt[k].x >= 0 && mt[k].z < t0 + PW) {
-#pragma unroll
-              for (int c = 0; c < PW; ++c)
-                if (t0 + c >= mt[k].z) v[k * PW + c] = -INFINITY;
+            for (int i = 0; i < kP; ++i) {
+              v[i] = k1 == 0 ? __uint_as_float(sr[i]) : -INFINITY;
+              v[kP + i] = k1 == 1 ? __uint_as_float(sr[i]) : -INFINITY;
             }
-            const float* w = v + k * PW;
-            float mk = fmax3(w[0], w[1], w[2]);
-#pragma unroll
-            for (int c = 3; c + 1 < PW; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
-            if constexpr (PW % 2 == 0) mk = fmaxf(mk, w[PW - 1]);
-            mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
           }
-          mx *= p.scale_log2;
-          const bool need = mx > m_ref + 8.0f;
-          if (__any_sync(0xffffffffu, need) && j > 0) {
-            if (r == 0) TTS_TR2(j, 7);
-            // every earlier PV product must have landed before O is rescaled in TMEM
-            bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
-            tc_fence_after();
-            const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#endif
+        }
+        // raw scores (scale > 0 commutes with max); rows not reading page k
+        // are masked once per page (max -> -inf, exponent offset -> -inf, so
+        // P is exactly 0); token slots >= ntok only on a partial page
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+          if (mt[k].x >= 0 && mt[k].z < kP) {
+#pragma unroll
+            for (int c = 0; c < kP; ++c)
+              if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
+          }
+          const float* w = v + k * kP;
+          float mk = fmax3(w[0], w[1], w[2]);
+#pragma unroll
+          for (int c = 3; c + 1 < kP; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
+          mk = fmaxf(mk, w[kP - 1]);
+          mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
+        }
+        mx *= p.scale_log2;
+        const bool need = mx > m_ref + 8.0f;
+        if (__any_sync(0xffffffffu, need) && j > 0) {
+          if (r == 0) TTS_TR2(j, 7);
+          // every earlier PV product must have landed before O is rescaled in TMEM
+          bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
+          tc_fence_after();
+          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
 #pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-              uint32_t o[32];
-              tc_ld32(t_o + lane_off + ch * 32, o);
-              tc_wait_ld();
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t o[32];
+            tc_ld32(t_o + lane_off + ch * 32, o);
+            tc_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tc_st32(t_o + lane_off + ch * 32, o);
-            }
-            tc_wait_st();
-            l *= alpha;
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tc_st32(t_o + lane_off + ch * 32, o);
           }
-          if (need) m_ref = mx;
-          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-          float2 lacc = make_float2(0.f, 0.f);
+          tc_wait_st();
+          l *= alpha;
+        }
+        if (need) m_ref = mx;
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int k = 0; k < NPG; ++k) {
-            if (wm[k]) {
-              const float nm = mem[k] ? -m_ref : -INFINITY;
-              const float2 nm2 = make_float2(nm, nm);
+        for (int k = 0; k < kU; ++k) {
+          if (wm[k]) {
+            const float nm = mem[k] ? -m_ref : -INFINITY;
+            const float2 nm2 = make_float2(nm, nm);
 #pragma unroll
-              for (int c = 0; c < PW; c += 2) {
-                const float2 x = ffma2(make_float2(v[k * PW + c], v[k * PW + c + 1]), sc2, nm2);
-                const float a = ex2(x.x), b = ex2(x.y);
-                lacc = fadd2(lacc, make_float2(a, b));
-                pk[(k * PW + c) / 2] = pack_f16x2(a, b);
+            for (int c = 0; c < kP; c += 2) {
+              const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
+              float a, b;
+              if (kPoly && ((c >> 1) & 1)) {
+                const float2 e2 = ex2_poly2(x);
+                a = e2.x;
+                b = e2.y;
+              } else {
+                a = ex2(x.x);
+                b = ex2(x.y);
               }
+              lacc = fadd2(lacc, make_float2(a, b));
+              pk[(k * kP + c) / 2] = pack_f16x2(a, b);
             }
           }
-          l += lacc.x + lacc.y;
         }
-        // P (fp16) over the unit's first 16 S columns (value c at column c/2):
-        // this copy's block [c0/2, c0/2 + CW/2), zeros in the other copies' blocks
-        const uint32_t tp = t_s + lane_off + (j & 1) * kSCols;
-        if constexpr (CW == 32) {
-          tc_st16(tp, pk);
-        } else if constexpr (CW == 16) {
-#pragma unroll
-          for (int bk = 0; bk < 2; ++bk) {
-            uint32_t d[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) d[i] = rep == bk ? pk[i] : 0u;
-            tc_st8(tp + bk * 8, d);
-          }
-        } else {
-#pragma unroll
-          for (int bk = 0; bk < 4; ++bk) {
-            uint32_t d[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) d[i] = rep == bk ? pk[i] : 0u;
-            tc_st4(tp + bk * 4, d);
-          }
-        }
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (r == 0) TTS_TR(j, 6);
-        if (lane == 0) TTS_TR2(j, warp);
-        if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
+        l += lacc.x + lacc.y;
       }
-    };
-    if (R == 4) {
-      loop(IntTag<8>{});
-    } else if (R == 2) {
-      loop(IntTag<16>{});
-    } else {
-      loop(IntTag<32>{});
+      // P (fp16) over the unit's first 16 S columns (value c at column c/2)
+      tc_st16(t_s + lane_off + (j & 1) * kSCols, pk);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (r == 0) TTS_TR(j, 6);
+      if (lane == 0) TTS_TR2(j, warp);
+      if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
     }
     const int n_done = j;
     // ---------------- epilogue ----------------
@@ -633,13 +675,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_wait(b_pv + 8 * ((n_done - 1) & 1), ((n_done - 1) >> 1) & 1u);
       tc_fence_after();
     }
-    float* op = reinterpret_cast<float*>(bp + kOffRing);  // the ring is idle now
-    auto swz = [](int row, int c) { return (c & ~7) | ((c & 7) ^ (row & 7)); };  // 16-B chunk c of a row
-    if (R == 1 && p.splits == 1) {
+    if (p.splits == 1) {
       if (n_done > 0) {
         const float inv = 1.f / l;
         float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq +
-                               kh * G + br % G) * kD;
+                               kh * G + rh) * kD;
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t o[32];
@@ -655,12 +695,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     } else {
-      // this copy's state -> smem, rescaled to the row's max over the R copies
+      // this slice's state (m, l, unnormalised O) -> smem for the cluster merge
+      float* op = reinterpret_cast<float*>(bp + kOffRing);  // the ring is idle now
       m_s[r] = m_ref;
-      if (R > 1) asm volatile("bar.sync 1, 128;" ::: "memory");
-      float M = m_ref;
-      for (int k = 0; k < R; ++k) M = fmaxf(M, m_s[br + k * RS]);
-      const float wgt = R > 1 ? exp2f(m_ref - M) : 1.f;
+      l_s[r] = l;
 #pragma unroll 1
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t o[32];
@@ -673,82 +711,30 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4) {
-          const int c = ch * 8 + q4;
-          *reinterpret_cast<float4*>(op + r * kD + swz(r, c) * 4) =
-              make_float4(__uint_as_float(o[4 * q4]) * wgt, __uint_as_float(o[4 * q4 + 1]) * wgt,
-                          __uint_as_float(o[4 * q4 + 2]) * wgt, __uint_as_float(o[4 * q4 + 3]) * wgt);
+          const int c = ch * 8 + q4;  // 16-B chunk of the row, XOR-swizzled against bank conflicts
+          *reinterpret_cast<float4*>(op + r * kD + ((c & ~7) | ((c & 7) ^ (r & 7))) * 4) =
+              make_float4(__uint_as_float(o[4 * q4]), __uint_as_float(o[4 * q4 + 1]),
+                          __uint_as_float(o[4 * q4 + 2]), __uint_as_float(o[4 * q4 + 3]));
         }
-      }
-      if (R > 1) {
-        l_s[r] = l * wgt;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        // the R copies of base row b2 summed by R threads, 128 / R columns each
-        const int b2 = r / R, cs = r % R;
-        const int nc4 = (kD / 4) / R;
-        float Mb = -INFINITY, Lb = 0.f;
-        for (int k = 0; k < R; ++k) {
-          Mb = fmaxf(Mb, m_s[b2 + k * RS]);
-          Lb += l_s[b2 + k * RS];
-        }
-        float4 acc[16];
-#pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4) {
-          acc[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (c4 < nc4) {
-            const int c = cs * nc4 + c4;
-            for (int k = 0; k < R; ++k) {
-              const int rr = b2 + k * RS;
-              const float4 x = *reinterpret_cast<const float4*>(op + rr * kD + swz(rr, c) * 4);
-              acc[c4].x += x.x;
-              acc[c4].y += x.y;
-              acc[c4].z += x.z;
-              acc[c4].w += x.w;
-            }
-          }
-        }
-        const int bl2 = b2 / G;
-        const bool ok2 = b2 < nrows && ((g.active >> bl2) & 1u);
-        if (p.splits == 1) {
-          if (ok2 && n_done > 0) {
-            const float inv = 1.f / Lb;
-            float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + bl2) * p.Hq +
-                                   kh * G + b2 % G) * kD;
-#pragma unroll
-            for (int c4 = 0; c4 < 16; ++c4)
-              if (c4 < nc4)
-                *reinterpret_cast<float4*>(orow + (cs * nc4 + c4) * 4) =
-                    make_float4(acc[c4].x * inv, acc[c4].y * inv, acc[c4].z * inv, acc[c4].w * inv);
-          }
-        } else {
-          // merged partial of base row b2 -> row b2 (only this thread touches
-          // its column slice of row b2) for the cluster merge
-#pragma unroll
-          for (int c4 = 0; c4 < 16; ++c4)
-            if (c4 < nc4) *reinterpret_cast<float4*>(op + b2 * kD + swz(b2, cs * nc4 + c4) * 4) = acc[c4];
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (cs == 0) {
-            m_s[b2] = Mb;
-            l_s[b2] = Lb;
-          }
-        }
-      } else {
-        l_s[r] = l;
       }
     }
   }
 
   if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
+  if (threadIdx.x == 0) TTS_CTA(1, gtimer());
   if (p.splits > 1) {
+    // a5: the S slices' partial states of every row merged through DSMEM;
+    // this CTA merges rows [split * 128 / S, (split + 1) * 128 / S)
     cluster_sync();
     if (warp < 4) {
       const int S = p.splits;
-      const int rpc = RS / S;  // base rows merged by this CTA
+      const int rpc = kRows / S;
       const int tpr = 128 / rpc;
       const int row = split * rpc + threadIdx.x / tpr;
       const int cseg = threadIdx.x % tpr;
       const int cw = kD / tpr;
-      const int bl = row / G;
-      const bool ok = row < nrows && ((g.active >> bl) & 1u) && !*s_bail;
+      int bl = 0, hd = 0;
+      const bool ok = row_of(row, bl, hd) && !*s_bail;
       const uint32_t lm = su32(m_s + row), ll = su32(l_s + row);
       // all remote loads of a step are issued before any is consumed (DSMEM
       // latency ~200 cycles; dependent loads would serialise)
@@ -769,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       const float inv = 1.f / L;
       float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + bl) * p.Hq +
-                             kh * G + row % G) * kD;
+                             kh * G + hd) * kD;
       for (int c4 = 0; c4 < cw / 4; ++c4) {
         const int c = cseg * (cw / 4) + c4;
         const int pc = (c & ~7) | ((c & 7) ^ (row & 7));
@@ -793,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
+  if (threadIdx.x == 0) TTS_CTA(2, gtimer());
   if (warp == 5) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -804,7 +791,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #ifdef TTS_TRACE
 extern "C" int tts_debug_read_trace(long long* out_h) {
   int e = (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
-  return e ? e : (int)cudaMemcpyFromSymbol(out_h + 1024 * 8, g_trace2, sizeof(g_trace2));
+  e = e ? e : (int)cudaMemcpyFromSymbol(out_h + 1024 * 8, g_trace2, sizeof(g_trace2));
+  return e ? e : (int)cudaMemcpyFromSymbol(out_h + 2 * 1024 * 8, g_cta, sizeof(g_cta));
 }
 #endif
 
@@ -814,8 +802,9 @@ bool umma_supported(const Ctx* c) {
 }
 
 int umma_max_beams(const Ctx* c) {
+  // four softmax warps, each holding whole beams (G lanes per beam)
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
-  return std::min(32, kRows / G);
+  return 4 * (32 / G);
 }
 
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
@@ -832,8 +821,10 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   pp.v_new = (const uint4*)v_new;
   pp.k_pool = (uint4*)c->buf.k_pool;
   pp.v_pool = (uint4*)c->buf.v_pool;
-  pp.items = c->ws_items;
-  pp.counts = c->ws_counts;
+  const int64_t rows = (int64_t)c->cfg.max_requests * c->cfg.max_beams;
+  pp.items = c->ws_items + c->plan_parity * rows * c->cfg.max_pages_per_beam;
+  pp.counts = c->ws_counts + c->plan_parity * rows;
+  c->plan_parity ^= 1;
   pp.n_groups = n_groups;
   pp.layer_begin = layer_begin;
   pp.n_call = n_call;
@@ -843,8 +834,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   pp.num_pages = c->cfg.num_pages;
 
   UParams p;
-  p.items = c->ws_items;
-  p.counts = c->ws_counts;
+  p.items = pp.items;
+  p.counts = pp.counts;
   p.q = q;
   p.out = out;
   p.groups = nullptr;
@@ -857,11 +848,6 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.maxB = c->cfg.max_beams;
   p.maxP = c->cfg.max_pages_per_beam;
   p.splits = splits;
-  // row copies (see the kernel): measured neutral-to-slower on C2 (the
-  // single MMA issuer, not the softmax, bounds the unit period), so off by
-  // default; TTS_ROW_COPIES=2|4 enables them
-  static const int copies = std::getenv("TTS_ROW_COPIES") ? std::atoi(std::getenv("TTS_ROW_COPIES")) : 1;
-  p.copies = copies >= 4 ? 4 : copies >= 2 ? 2 : 1;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
   UInline inl;  // host staging of the parameter block (copied by the launch)
@@ -877,13 +863,18 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     pp.groups = (const GroupDesc*)dg;
     pp.glens = (const int32_t*)dl;
   }
+  // measured 2% slower on C2/C3 (the softmax is latency-, not MUFU-bound): off unless TTS_POLY=1
+  static const bool poly = std::getenv("TTS_POLY") && std::atoi(std::getenv("TTS_POLY")) != 0;
+  auto kern = poly ? k_tree_umma<true> : k_tree_umma<false>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k_tree_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    if (e != cudaSuccess) return e;
-    // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
-    e = cudaFuncSetAttribute(k_tree_umma, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
+    for (auto k : {k_tree_umma<true>, k_tree_umma<false>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      if (e != cudaSuccess) return e;
+      // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+    }
     attr_done = true;
   }
   static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
@@ -916,7 +907,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   attr[1] = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = no_pdl ? 1 : 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_tree_umma, c->tmap_k, c->tmap3_v, p, inl);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, c->tmap_k, c->tmap3_v, p, inl);
   c->launches++;
   return e;
 }

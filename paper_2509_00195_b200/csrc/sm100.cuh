@@ -188,6 +188,24 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x for a pair on the FMA/ALU pipes (no MUFU): round-to-nearest split
+// x = r + f, f in [-0.5, 0.5], 2^f by a degree-3 polynomial (max relative error
+// 7.7e-5, below the fp16 rounding of P), 2^r added to the exponent field.  x is
+// clamped at -126 (the result is then <= 2^-126, i.e. 0 once rounded to fp16).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 mg = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: t = mg + round(x)
+  const float2 t = fadd2(x, mg);
+  const float2 f = fadd2(x, fadd2(mg, make_float2(-t.x, -t.y)));
+  float2 p = ffma2(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
+  p = ffma2(p, f, make_float2(0.69327624f, 0.69327624f));
+  p = ffma2(p, f, make_float2(0.99992894f, 0.99992894f));
+  // 2^round(x): (t_bits - mg_bits) << 23 == t_bits << 23 mod 2^32 (the low 9 bits of mg_bits are 0)
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

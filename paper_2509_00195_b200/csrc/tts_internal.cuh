@@ -81,8 +81,11 @@ struct Ctx {
   CUtensorMap tmap3_k, tmap3_v;
   bool tmap3_ok = false;
   // attention plan (a3): per-group distinct-page lists
-  int4* ws_items = nullptr;   // [max_requests * max_beams * max_pages_per_beam]
-  int32_t* ws_counts = nullptr;  // [max_requests * max_beams]
+  // two buffers, alternating per call, so that the next call's k_plan may run
+  // while this call's attention kernel still reads its plan
+  int4* ws_items = nullptr;      // [2][max_requests * max_beams * max_pages_per_beam]
+  int32_t* ws_counts = nullptr;  // [2][max_requests * max_beams]
+  int plan_parity = 0;
 };
 
 // ---- pool value format --------------------------------------------------------
@@ -102,9 +105,13 @@ __device__ __forceinline__ bool bf16x2_beyond_f16(uint32_t u) {
   const uint32_t el = (u >> 7) & 0xFF, eh = (u >> 23) & 0xFF;
   return (el >= 0x8F && el < 0xFF) || (eh >= 0x8F && eh < 0xFF);
 }
+// (a value with no fp16 representation is stored as 0 next to the sticky error,
+// so the pool never holds a non-finite V: masked columns multiply it by P = 0)
 __device__ __forceinline__ uint4 v_to_pool(uint4 v, int32_t* status) {
-  if (bf16x2_beyond_f16(v.x) | bf16x2_beyond_f16(v.y) | bf16x2_beyond_f16(v.z) | bf16x2_beyond_f16(v.w))
+  if (bf16x2_beyond_f16(v.x) | bf16x2_beyond_f16(v.y) | bf16x2_beyond_f16(v.z) | bf16x2_beyond_f16(v.w)) {
     atomicExch(status, (int32_t)TTS_ERR_UNSUPPORTED);
+    return make_uint4(0, 0, 0, 0);
+  }
   return make_uint4(bf16x2_to_f16x2(v.x), bf16x2_to_f16x2(v.y), bf16x2_to_f16x2(v.z), bf16x2_to_f16x2(v.w));
 }
 

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtts.so")
+LIB_PATH = os.environ.get("TTS_LIB_PATH") or os.path.join(HERE, "libtts.so")  # override: variant builds (tools/)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tts.h")
 
 

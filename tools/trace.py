@@ -16,10 +16,25 @@ cfg = workload.CONFIGS[name].with_(n_steps=int(sys.argv[1]) if len(sys.argv) > 1
 r = BeamStepRunner(cfg)
 r.run()
 import torch; torch.cuda.synchronize()
-trr = np.zeros((2, 1024, 8), dtype=np.int64)
+buf = np.zeros(2 * 1024 * 8 + 4096 * 4, dtype=np.int64)
 L = tts.load()
-L.tts_debug_read_trace(trr.ctypes.data_as(ctypes.c_void_p))
+L.tts_debug_read_trace(buf.ctypes.data_as(ctypes.c_void_p))
+trr = buf[:2 * 1024 * 8].reshape(2, 1024, 8)
 tr, t2 = trr[0], trr[1]
+cta = buf[2 * 1024 * 8:].reshape(4096, 4)
+cta = cta[cta[:, 0] > 0]
+if len(cta):
+    t0c = cta[:, 0].min()
+    st, le, ex = (cta[:, 0] - t0c) / 1e3, (cta[:, 1] - t0c) / 1e3, (cta[:, 2] - t0c) / 1e3
+    un = cta[:, 3] & 0xffffffff
+    sm = cta[:, 3] >> 32
+    print(f"last launch: {len(cta)} CTAs, span {ex.max():.1f} us; start min/med/max {st.min():.1f}/{np.median(st):.1f}/{st.max():.1f};"
+          f" exit min/med/max {ex.min():.1f}/{np.median(ex):.1f}/{ex.max():.1f}; units min/med/max {un.min()}/{int(np.median(un))}/{un.max()}")
+    dur = ex - st
+    print(f"  CTA duration min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us; us per unit (median) {np.median(dur / np.maximum(un, 1)):.3f};"
+          f" epilogue (exit - loop end) median {np.median(ex - le):.2f} us; distinct SMs {len(set(sm.tolist()))}")
+    hist = np.histogram(ex, bins=10)
+    print("  exit-time histogram:", hist[0].tolist(), "edges", [round(x, 1) for x in hist[1].tolist()])
 n = int((tr[:, 4] > 0).sum())
 t0 = tr[0, 4]
 print("units", n)
