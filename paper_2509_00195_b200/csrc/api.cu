@@ -27,6 +27,8 @@ size_t workspace_bytes(const tts_config_t& c) {
   s += align_up((size_t)c.num_pages * 4);           // stats marks
   s += align_up(2 * rows * c.max_pages_per_beam * 16);  // attention plan items (double-buffered)
   s += align_up(2 * rows * 4);                          // plan counts
+  s += align_up(umma_partial_bytes());                  // split tiles' partial states
+  s += align_up((size_t)c.num_layers * c.num_kv_heads * umma_max_groups() * 4);  // split-tile counters
   s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
   return s;
 }
@@ -160,6 +162,11 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   w += tts::align_up(2 * rws * cfg->max_pages_per_beam * 16);
   c->ws_counts = (int32_t*)w;
   w += tts::align_up(2 * rws * 4);
+  c->ws_partial = (float*)w;
+  w += tts::align_up(tts::umma_partial_bytes());
+  c->ws_tile_cnt = (int32_t*)w;
+  const size_t cnt_bytes = (size_t)cfg->num_layers * cfg->num_kv_heads * tts::umma_max_groups() * 4;
+  w += tts::align_up(cnt_bytes);
   c->ws_upload = w;
   if (cudaMallocHost(&c->pinned, (size_t)tts::kUploadSlots * tts::kUploadSlotBytes) != cudaSuccess) {
     delete c;
@@ -170,7 +177,8 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
     tts_destroy(c);
     return TTS_ERR_CUDA;
   }
-  if (tts::launch_init_state(c, 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
+  if (cudaMemsetAsync(c->ws_tile_cnt, 0, cnt_bytes, 0) != cudaSuccess ||
+      tts::launch_init_state(c, 0) != cudaSuccess || cudaStreamSynchronize(0) != cudaSuccess) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
   }
@@ -356,21 +364,14 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
   const bool use_umma = tts::umma_supported(c) && !(path && std::strcmp(path, "mma") == 0);
   std::vector<tts::GroupDesc> groups;
   if (use_umma) {
-    // 128-row tiles: balanced runs of <= floor(128/G) beams; positions split
-    // across a cluster when the grid would not fill the GPU
-    // Tile shape: the largest beam groups (most page sharing per CTA) that
-    // still put >= 3/4 of a wave (2 CTAs per SM) on the GPU; only when even
-    // single-beam groups cannot, split each tile's page list over a cluster.
-    // Measured (C2, one request per call): 4-beam groups, no split, 40 us vs
-    // 16-beam groups split 4 ways, 47 us -- the cluster merge waits on the
-    // slowest slice.
-    // Tile shape: the largest beam groups (most page sharing per CTA) that
-    // still put >= 3/4 of a wave (2 CTAs per SM) on the GPU; only when even
-    // single-beam groups cannot, split each tile's page list over a cluster.
-    // Measured: C2 (16 beams, one request per call) 4-beam groups, no split,
-    // 40 us vs 16-beam groups split 4 ways, 47 us (the cluster merge waits on
-    // the slowest slice); C3 (64 beams) 16-beam groups (448 CTAs) beat the
-    // better-quantised 13-beam groups (560 CTAs) by 3%.
+    // 128-row tiles: balanced runs of <= umma_max_beams beams of one request.
+    // The largest groups (a page shared inside a group is staged once) that
+    // still give >= 3/4 of a round of tiles for the 2 CTAs per SM of the
+    // persistent kernel; a smaller remainder is split over all CTAs there
+    // (stream-K).  Measured (C2, one request per call): 4-beam groups, 224
+    // whole tiles, 40 us per call vs 16-beam groups, 56 tiles split ~5 ways,
+    // 59 us (the split pieces cost unequal time: the shared prefix at the head
+    // of a tile keeps all four softmax warps busy, a private tail one).
     int maxb = tts::umma_max_beams(c);
     if (const char* s = std::getenv("TTS_GROUP_BEAMS")) maxb = std::max(1, std::min(maxb, std::atoi(s)));
     const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;
@@ -384,28 +385,23 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
       return gb;
     };
     int gb = group_size(maxb);
-    std::vector<int32_t> glens;
-    plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
-    if (groups.empty()) return TTS_OK;
+    plan_groups(c, n_req, req_ids, active, gb, groups);
     if (!std::getenv("TTS_GROUP_BEAMS")) {
       while (gb > 1 && (int64_t)groups.size() * g.num_kv_heads * n_layers < want) {
         gb = group_size((gb + 1) / 2);
-        plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
+        plan_groups(c, n_req, req_ids, active, gb, groups);
       }
     }
-    const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
-    int splits = 1;
-    if (const char* s = std::getenv("TTS_SPLITS")) {
-      splits = std::max(1, std::min(8, std::atoi(s)));
-    } else {
-      while (splits < 8 && ctas * splits < want) splits *= 2;
-    }
+    std::vector<int32_t> glens;
+    plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
+    if (groups.empty()) return TTS_OK;
+    if ((int)groups.size() > tts::umma_max_groups()) return TTS_ERR_CAPACITY;
     const bool append = pending && !pending->empty();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) prof_pair(c, &e0, &e1);
     if (e0) TTS_CUDA(cudaEventRecord(e0, st));
     TTS_CUDA(tts::launch_attention_umma(c, groups.data(), (int)groups.size(), glens.data(), (int)glens.size(),
-                                        splits, layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out,
+                                        layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out,
                                         append ? (const __nv_bfloat16*)k_new : nullptr,
                                         append ? (const __nv_bfloat16*)v_new : nullptr, st));
     if (e1) TTS_CUDA(cudaEventRecord(e1, st));

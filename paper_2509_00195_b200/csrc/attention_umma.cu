@@ -52,16 +52,16 @@ constexpr int kThreads = 224;                // warps 0-3 softmax, 4 producer, 5
 constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
 constexpr int kSCols = kU * kP;              // 32
 
+constexpr int kMaxGroups = 1024;             // beam groups per call (smem prefix of their unit counts)
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 8;        // full, empty, sfull[2], pfull[2], pv[2], qready, append
-constexpr int kOffML = kOffBar + kNumBars * 8 + 16;
-constexpr int kScrItems = 512;               // plan scratch: W positions x <= nb runs, W * nb <= 512
-constexpr int kOffScr = kOffML + 2 * kRows * 4;
-constexpr int kOffLen = kOffScr + kScrItems * 16;
-constexpr int kSmemBytes = kOffLen + 32 * 4 + 1024;
-static_assert(kRing >= kRows * kD * 4, "merge area must hold a 128x128 fp32 tile");
+constexpr int kNumBars = 2 * kNS + 8;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree
+constexpr int kOffScr = kOffBar + kNumBars * 8 + 16;
+constexpr int kScrItems = 64;                // producer: one batch of 32 units (2 items each)
+constexpr int kOffPre = kOffScr + kScrItems * 16;
+constexpr int kOffInfo = kOffPre + (kMaxGroups + 1) * 4;
+constexpr int kSmemBytes = kOffInfo + 16 + 1024;
 static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
 
 #ifdef TTS_TRACE
@@ -108,10 +108,14 @@ struct UParams {
   const GroupDesc* groups;    // device copies when the call does not fit the parameter block,
                               // else null (descriptors in UInline)
   int32_t* status;
-  int layer_begin, n_call, Hq, Hkv, G, maxB, maxP, splits;
+  float* partial;             // [2 * gridDim.x][m 128 | l 128 | O 128 x 128]: split tiles' partial states
+  int32_t* tile_cnt;          // [n_tiles] pieces of a split tile done (reset by its merger)
+  int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
   int64_t num_pages;
   float scale_log2;
 };
+constexpr int kPartFloats = 2 * kRows + kRows * kD;
+constexpr int kMaxCtas = 2 * 160;  // partial-state slots are sized for this many CTAs
 
 // The call's descriptors in the kernel parameter block (no H2D copy on the stream)
 constexpr int kInlineGroups = 32;
@@ -293,8 +297,18 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 }
 
 // ---------------------------------------------------------------------------
+// Persistent attention (a4 + a5), 2 CTAs per SM.  The call's work is a
+// sequence of units (2 distinct pages of one tile), tiles ordered (layer, kv
+// head, group) with the group fastest.  Whole tiles go round-robin while there
+// are at least 3/4 as many left as CTAs (phase 1); the units of the rest are
+// split evenly over the CTAs (phase 2, stream-K).  A CTA's phase-2 range covers whole
+// tiles and at most two partial ones; a tile split over several CTAs is merged
+// by the CTA that finishes its piece last (global counter), reading the
+// pieces' partial (m, l, O) in piece order, so the result does not depend on
+// which CTA finishes first.  Every warp derives the same piece sequence from
+// the per-group unit counts (prefix in smem).
 // kPoly: every other pair of exponentials on the FMA/ALU pipes (ex2_poly2)
-// instead of MUFU, halving the softmax warps' MUFU occupancy
+// instead of MUFU.
 template <bool kPoly>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
@@ -306,28 +320,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   int4* meta = reinterpret_cast<int4*>(bp + kOffMeta);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bp + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  float* m_s = reinterpret_cast<float*>(bp + kOffML);
-  float* l_s = m_s + kRows;
   int4* scr = reinterpret_cast<int4*>(bp + kOffScr);
-  int* s_bail = reinterpret_cast<int*>(bp + kOffLen);
+  int* s_pre = reinterpret_cast<int*>(bp + kOffPre);  // [n_groups + 1] exclusive prefix of units per group
+  int* s_info = reinterpret_cast<int*>(bp + kOffInfo);  // [0] merger flag
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16;
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_ofree = b_qready + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
   if (threadIdx.x == 0) TTS_CTA(0, gtimer());
   // the next call's k_plan may start as soon as every CTA of this grid runs
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
-  // Programmatic dependent launch: this grid starts while k_plan (the call's
-  // append + plan) runs.  The prologue below (barriers, TMEM, Q -> TMEM) reads
-  // nothing k_plan writes; the producer warp alone waits (griddepcontrol.wait)
-  // before it reads the plan, the pool or the status word.
-  const int split = blockIdx.x % p.splits;
-  const int gidx = blockIdx.x / p.splits;
-  const GroupDesc g = p.groups ? p.groups[gidx] : inl.g[gidx];
-  const int kh = blockIdx.y, lrel = blockIdx.z, layer = p.layer_begin + lrel;
-  const int G = p.G;
-
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNS; ++i) {
       bar_init(b_full + 8 * i, 1);
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       bar_init(b_pv + 8 * i, 1);
     }
     bar_init(b_qready, 4);
-    *s_bail = 0;
+    bar_init(b_ofree, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -347,131 +350,214 @@ __global__ void __launch_bounds__(kThreads, 2)
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // Rows of the tile, balanced over the four lane quadrants (softmax warps):
-  // warp w holds beams [w*bpw, (w+1)*bpw) of the group, G consecutive lanes
-  // per beam (host: bpw * G <= 32).  A page's exponentials are computed only by
-  // the warps holding one of its member beams, so spreading the beams evenly
-  // spreads the softmax work of private pages over all four warps.
-  const int bpw = (g.nbeams + 3) >> 2;
-  auto row_of = [&](int row, int& beam, int& head) {
-    const int l = row & 31, bw = l / G;
-    beam = (row >> 5) * bpw + bw;
-    head = l - bw * G;
-    return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
-  };
-  const int r = threadIdx.x;
-  int rbl = 0, rh = 0;
-  const bool rvalid = warp < 4 && row_of(r, rbl, rh);
-  uint32_t qv[64];  // this thread's query row (bf16 pairs), loaded before the TMEM handshake
-  if (warp < 4) {
-    const uint4* src = reinterpret_cast<const uint4*>(
-        p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (rvalid ? rbl : 0)) * p.Hq + kh * G +
-               (rvalid ? rh : 0)) * kD);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const uint4 v = rvalid ? src[c] : make_uint4(0, 0, 0, 0);
-      qv[4 * c] = v.x;
-      qv[4 * c + 1] = v.y;
-      qv[4 * c + 2] = v.z;
-      qv[4 * c + 3] = v.w;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_o = tmem, t_q = tmem + 128, t_s = tmem + 192;
-  if (warp < 4) {
-    // Q tile -> TMEM (the A operand of S = Q K^T): lane = row, column = d pair
-    const uint32_t lo = (uint32_t)(warp * 32) << 16;
-    uint32_t h0[32], h1[32];
+  const int G = p.G;
+  const int ng = p.n_groups;
+  const int T = p.n_layers * p.Hkv * ng;
+  const int Cg = gridDim.x;
+  // whole-tile rounds (phase 1); a last round that would fill >= 3/4 of the
+  // CTAs is also taken whole (cheaper than splitting and merging every tile)
+  int k1 = T / Cg;
+  if (4 * (T - k1 * Cg) >= 3 * Cg) ++k1;
+  const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
+  auto group_of = [&](int gi) { return p.groups ? p.groups[gi] : inl.g[gi]; };
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const int r = threadIdx.x;
+  // Rows of a tile, balanced over the four lane quadrants (softmax warps):
+  // warp w holds beams [w*bpw, (w+1)*bpw) of the group, G consecutive lanes
+  // per beam (host: bpw * G <= 32).  A page's exponentials are computed only
+  // by the warps holding one of its member beams, so spreading the beams
+  // evenly spreads the softmax work of private pages over all four warps.
+  auto row_of = [&](const GroupDesc& g, int row, int& beam, int& head) {
+    const int bpw = (g.nbeams + 3) >> 2;
+    const int l = row & 31, bw = l / G;
+    beam = (row >> 5) * bpw + bw;
+    head = l - bw * G;
+    return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
+  };
+  // Q rows of a piece -> TMEM (the A operand of S = Q K^T): lane = row, column = d pair
+  auto load_q = [&](int gi, int slab) {
+    const GroupDesc g = group_of(gi);
+    int bl, hd;
+    const bool ok = row_of(g, r, bl, hd);
+    const int lrel = slab / p.Hkv, kh = slab % p.Hkv;
+    const uint4* src = reinterpret_cast<const uint4*>(
+        p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (ok ? bl : 0)) * p.Hq + kh * G +
+               (ok ? hd : 0)) * kD);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      h0[i] = qv[i];
-      h1[i] = qv[32 + i];
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t h[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = ok ? __ldg(src + hf * 8 + c) : make_uint4(0, 0, 0, 0);
+        h[4 * c] = v.x;
+        h[4 * c + 1] = v.y;
+        h[4 * c + 2] = v.z;
+        h[4 * c + 3] = v.w;
+      }
+      tc_st32(t_q + lane_off + hf * 32, h);
     }
-    tc_st32(t_q + lo, h0);
-    tc_st32(t_q + lo + 32, h1);
     tc_wait_st();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) bar_arrive(b_qready);  // the MMA warp may start S = Q K^T
+    if (lane == 0) bar_arrive(b_qready);
+  };
+  // the first phase-1 tile (blockIdx.x) is known without the plan: its Q goes
+  // to TMEM while k_plan still runs (q is not written by k_plan)
+  if (warp < 4 && n1 > 0) load_q((int)blockIdx.x % ng, (int)blockIdx.x / ng);
+  // Programmatic dependent launch: this grid starts while k_plan (the call's
+  // append + plan) runs; everything below reads what k_plan writes.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (warp == 0) {
+    const bool bail = *(volatile int32_t*)p.status != 0;  // sticky error: no work (outputs untouched)
+    int run = 0;
+    for (int i0 = 0; i0 < p.n_groups; i0 += 32) {
+      const int i = i0 + lane;
+      const int u = (i < p.n_groups && !bail) ? (__ldg(p.counts + i) + 1) / 2 : 0;
+      int x = u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < p.n_groups) s_pre[i + 1] = run + x;
+      run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) s_pre[0] = 0;
   }
-
-  if (threadIdx.x == 0) TTS_TR(1023, 1);  // prologue done (Q in TMEM)
+  __syncthreads();
+  const int S = s_pre[p.n_groups];  // units per (layer, kv head) slab
+  const int64_t U = (int64_t)S * p.n_layers * p.Hkv;
+  // Schedule.  Tiles t = slab * ng + gi (slab = layer * Hkv + kv head).
+  // Phase 1: k1 rounds of whole tiles, tile blockIdx.x + k * C in round k --
+  // the groups of one slab run side by side, so pages they share are read
+  // from HBM about once (L2).  Phase 2: the units of the remaining tiles, split
+  // over the CTAs (stream-K).
+  auto F = [&](int t) { return (int64_t)(t / ng) * S + s_pre[t % ng]; };  // first unit of tile t
+  const int64_t base2 = F(min(k1 * Cg, T));
+  const int64_t U2 = U - base2;
+  // phase-2 CTAs: every one gets >= 1 unit (a split tile's pieces are then
+  // exactly the CTAs whose ranges meet it)
+  // Balanced split (when phase 1 ran and every tile is smaller than a CTA's
+  // fair share U / C): CTA c's phase-2 range tops its phase-1 tiles up to
+  // ~(c+1) U / C units in total, start2(c) = base2 + c U / C - (phase-1 units
+  // of CTAs < c).  Otherwise an even split of the phase-2 units.
+  int maxu = 0;
+  for (int i = 0; i < ng; ++i) maxu = max(maxu, s_pre[i + 1] - s_pre[i]);
+  const bool bal = k1 > 0 && U2 > 0 && (int64_t)k1 * maxu + 1 <= U / Cg;
+  const int C2 = bal ? Cg : (int)min((int64_t)Cg, U2);
+  auto f1 = [&](int cc) {  // phase-1 units of CTAs [0, cc)
+    int64_t a = 0;
+    for (int k = 0; k < k1; ++k) a += F(min(cc + k * Cg, T)) - F(min(k * Cg, T));
+    return a;
+  };
+  auto start2 = [&](int cc) {
+    return bal ? base2 + (int64_t)cc * U / Cg - f1(cc) : base2 + (int64_t)cc * U2 / C2;
+  };
+  const int64_t ua2 = (int)blockIdx.x < C2 ? start2(blockIdx.x) : 0;
+  const int64_t ub2 = (int)blockIdx.x < C2 ? start2(blockIdx.x + 1) : 0;
+  // the tile piece containing global unit u (phase 2): units [j0, j1) of tile (slab, gi)
+  auto piece_at = [&](int64_t u, int& gi, int& slab, int& j0, int& j1) {
+    slab = (int)(u / S);
+    const int o = (int)(u - (int64_t)slab * S);
+    int lo = 0, hi = ng;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= o) lo = mid;
+      else hi = mid;
+    }
+    gi = lo;
+    j0 = o - s_pre[gi];
+    j1 = (int)min((int64_t)(s_pre[gi + 1] - s_pre[gi]), (int64_t)j0 + (ub2 - u));
+  };
+  int n_pieces = n1;
+  for (int64_t u = ua2; u < ub2; ++n_pieces) {
+    int gi, slab, j0, j1;
+    piece_at(u, gi, slab, j0, j1);
+    u += j1 - j0;
+  }
+  // piece idx of this CTA; pslot: partial-state slot (-1: phase 1, whole tile)
+  auto piece = [&](int idx, int& gi, int& slab, int& j0, int& j1, int& pslot) {
+    if (idx < n1) {
+      const int t = blockIdx.x + idx * Cg;
+      slab = t / ng;
+      gi = t - slab * ng;
+      j0 = 0;
+      j1 = s_pre[gi + 1] - s_pre[gi];
+      pslot = -1;
+      return;
+    }
+    int64_t u = ua2;
+    for (int q = idx - n1;; --q) {
+      piece_at(u, gi, slab, j0, j1);
+      if (q == 0) break;
+      u += j1 - j0;
+    }
+    pslot = 2 * blockIdx.x + (u == ua2 ? 0 : 1);
+  };
 
   if (warp == 4) {
     // ========================= producer: TMA =========================
-    // Units = consecutive pairs of the group's plan items (k_plan, a3); with a
-    // cluster split this CTA takes a contiguous, balanced range of them.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const bool bail = *(volatile int32_t*)p.status != 0;
-    const int nit = bail ? 0 : p.counts[gidx];
-    const int n_units = (nit + 1) / 2;
-#ifdef TTS_TRACE
-    if (lane == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      TTS_CTA(3, (long long)n_units | ((long long)smid << 32));
-    }
-#endif
-    const int u_lo = (int)((int64_t)split * n_units / p.splits);
-    const int u_hi = (int)((int64_t)(split + 1) * n_units / p.splits);
-    const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
-    const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
     int slot = 0;
     uint32_t ph = 0;
-    auto issue = [&](const int4& m0, const int4& m1) {  // lane 0
-      bar_wait(b_empty + 8 * slot, ph ^ 1u);
-      meta[slot * kU] = m0;
-      meta[slot * kU + 1] = m1;
-      const uint32_t fb = b_full + 8 * slot;
-      bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
-      const uint32_t sb = base + kOffRing + slot * kSlot;
-      // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
-      // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
-      const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
-      tma2d(sb, &tmk, 0, y0, fb);
-      tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
-      tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
-      if (m1.x >= 0) {
-        const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
-        tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
-        tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
-        tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+    for (int pc = 0; pc < n_pieces; ++pc) {
+      int gi, slab, j0, j1, pslot;
+      piece(pc, gi, slab, j0, j1, pslot);
+      const GroupDesc g = group_of(gi);
+      const int kh = slab % p.Hkv, layer = p.layer_begin + slab / p.Hkv;
+      const int nit = __ldg(p.counts + gi);
+      const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
+      const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
+      auto issue = [&](const int4& m0, const int4& m1) {  // lane 0
+        bar_wait(b_empty + 8 * slot, ph ^ 1u);
+        meta[slot * kU] = m0;
+        meta[slot * kU + 1] = m1;
+        const uint32_t fb = b_full + 8 * slot;
+        bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
+        const uint32_t sb = base + kOffRing + slot * kSlot;
+        // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
+        // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
+        const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
+        tma2d(sb, &tmk, 0, y0, fb);
+        tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
+        tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
+        if (m1.x >= 0) {
+          const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
+          tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
+          tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
+          tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+        }
+        if (++slot == kNS) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      };
+      // 32 units per batch (lane = unit); the next batch's loads are in
+      // flight while lane 0 issues the current one
+      int4 a0 = make_int4(-2, 0, 0, 0), a1 = a0;
+      auto load = [&](int v0) {
+        const int v = v0 + lane;
+        if (v < j1) {
+          a0 = __ldg(its + 2 * v);
+          a1 = 2 * v + 1 < nit ? __ldg(its + 2 * v + 1) : make_int4(-2, 0, 0, 0);
+        }
+      };
+      load(j0);
+      for (int v0 = j0; v0 < j1; v0 += 32) {
+        scr[2 * lane] = a0;
+        scr[2 * lane + 1] = a1;
+        __syncwarp();
+        if (v0 + 32 < j1) load(v0 + 32);
+        if (lane == 0) {
+          const int n = min(32, j1 - v0);
+          for (int k = 0; k < n; ++k) issue(scr[2 * k], scr[2 * k + 1]);
+        }
+        __syncwarp();
       }
-      if (++slot == kNS) {
-        slot = 0;
-        ph ^= 1u;
-      }
-    };
-    // 32 units per batch (lane = unit); the next batch's loads are in flight
-    // while lane 0 issues the current one
-    int4 a0 = make_int4(-2, 0, 0, 0), a1 = a0;
-    auto load = [&](int u0) {
-      const int u = u0 + lane;
-      if (u < u_hi) {
-        a0 = its[2 * u];
-        a1 = 2 * u + 1 < nit ? its[2 * u + 1] : make_int4(-2, 0, 0, 0);
-      }
-    };
-    load(u_lo);
-    for (int u0 = u_lo; u0 < u_hi; u0 += 32) {
-      scr[2 * lane] = a0;
-      scr[2 * lane + 1] = a1;
-      __syncwarp();
-      if (u0 + 32 < u_hi) load(u0 + 32);
-      if (lane == 0) {
-        const int n = min(32, u_hi - u0);
-        for (int k = 0; k < n; ++k) issue(scr[2 * k], scr[2 * k + 1]);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) {
-      if (bail) *s_bail = 1;
-      bar_wait(b_empty + 8 * slot, ph ^ 1u);
-      meta[slot * kU] = make_int4(-1, 0, 0, 0);
-      bar_arrive(b_full + 8 * slot);
     }
   } else if (warp == 5) {
     // ========================= S issuer: S = Q K^T =========================
@@ -480,206 +566,219 @@ __global__ void __launch_bounds__(kThreads, 2)
     // waits behind the other's issue (the tensor pipe runs both in issue order).
     constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
     const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);  // K tiles: K-major SW128
-    bar_wait(b_qready, 0);  // Q in TMEM
-    for (int j = 0;; ++j) {
-      const int slot = j % kNS;
-      if (lane == 0) TTS_TR(j, 0);
-      bar_wait(b_full + 8 * slot, (j / kNS) & 1u);
-      if (lane == 0) TTS_TR(j, 1);
-      tc_fence_after();
-      if (meta[slot * kU].x == -1) {
-        if (elect_one()) bar_arrive(b_sfull + 8 * (j & 1));  // the softmax warps see the sentinel
-        __syncwarp();
-        break;
-      }
-      // S buffer j & 1 holds P(j - 2) until PV(j - 2) has read it
-      if (j >= 2) bar_wait(b_pv + 8 * (j & 1), ((j - 2) >> 1) & 1u);
-      tc_fence_after();
-      // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
-      // absent second page leaves columns 16..31 undefined; they are masked)
-      const uint32_t sd = t_s + (j & 1) * kSCols;
-      const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
-      if (elect_one()) {
+    int js = 0;
+    for (int pc = 0; pc < n_pieces; ++pc) {
+      int gi, slab, j0, j1, pslot;
+      piece(pc, gi, slab, j0, j1, pslot);
+      bar_wait(b_qready, pc & 1);  // this piece's Q in TMEM
+      for (int j = j0; j < j1; ++j, ++js) {
+        const int slot = js % kNS;
+        if (lane == 0) TTS_TR(js, 0);
+        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        if (lane == 0) TTS_TR(js, 1);
+        // S buffer js & 1 holds P(js - 2) until PV(js - 2) has read it
+        if (js >= 2) bar_wait(b_pv + 8 * (js & 1), ((js - 2) >> 1) & 1u);
+        tc_fence_after();
+        // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
+        // absent second page leaves columns 16..31 undefined; they are masked)
+        const uint32_t sd = t_s + (js & 1) * kSCols;
+        const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks)
-          mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s, ks > 0);
-        tc_commit(b_sfull + 8 * (j & 1));
+          for (int ks = 0; ks < kD / 16; ++ks)
+            mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s, ks > 0);
+          tc_commit(b_sfull + 8 * (js & 1));
+        }
+        __syncwarp();
+        if (lane == 0) TTS_TR(js, 7);
       }
-      __syncwarp();
-      if (lane == 0) TTS_TR(j, 7);
     }
   } else if (warp == 6) {
     // ====================== PV issuer: O += P V ======================
     constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
     const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
-    uint32_t acc = 0;
-    for (int j = 0;; ++j) {
-      const int slot = j % kNS;
-      bar_wait(b_full + 8 * slot, (j / kNS) & 1u);
-      if (meta[slot * kU].x == -1) break;
-      bar_wait(b_pfull + 8 * (j & 1), (j >> 1) & 1u);
-      if (lane == 0) TTS_TR(j, 2);
-      tc_fence_after();
-      const uint32_t pa = t_s + (j & 1) * kSCols;
-      const bool e = elect_one();
+    int js = 0;
+    for (int pc = 0; pc < n_pieces; ++pc) {
+      int gi, slab, j0, j1, pslot;
+      piece(pc, gi, slab, j0, j1, pslot);
+      for (int j = j0; j < j1; ++j, ++js) {
+        const int slot = js % kNS;
+        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        bar_wait(b_pfull + 8 * (js & 1), (js >> 1) & 1u);
+        // the first PV of a piece overwrites O: the previous piece's epilogue must have read it
+        if (j == j0 && pc > 0) bar_wait(b_ofree, (pc - 1) & 1);
+        if (lane == 0) TTS_TR(js, 2);
+        tc_fence_after();
+        const uint32_t pa = t_s + (js & 1) * kSCols;
+        const bool e = elect_one();
+        uint32_t acc = j != j0;
 #pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        if (meta[slot * kU + k].x < 0) continue;
-        const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
-        if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
-        acc = 1;
+        for (int k = 0; k < kU; ++k) {
+          if (meta[slot * kU + k].x < 0) continue;
+          const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
+          if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
+          acc = 1;
+        }
+        if (e) {
+          // S(js) completed before the softmax produced P(js), so this commit
+          // covers every read of the slot
+          tc_commit(b_empty + 8 * slot);
+          tc_commit(b_pv + 8 * (js & 1));
+          TTS_TR(js, 3);
+        }
+        __syncwarp();
       }
-      if (e) {
-        // S(j) completed before the softmax produced P(j), so this commit
-        // covers every read of the slot
-        tc_commit(b_empty + 8 * slot);
-        tc_commit(b_pv + 8 * (j & 1));
-        TTS_TR(j, 3);
-      }
-      __syncwarp();
     }
   } else if (warp < 4) {
     // ============================ softmax (warps 0-3) ============================
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    float m_ref = -1e30f, l = 0.f;
-    int j = 0;
-    for (;; ++j) {
-      if (r == 0) TTS_TR(j, 4);
-      bar_wait(b_sfull + 8 * (j & 1), (j >> 1) & 1u);
-      if (r == 0) TTS_TR(j, 5);
-      tc_fence_after();
-      const int slot = j % kNS;
-      if (meta[slot * kU].x == -1) break;
-      int4 mt[kU];
-      bool mem[kU], wm[kU];
-      bool wany = false;
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        mt[k] = meta[slot * kU + k];
-        // warp-uniform page membership: a warp none of whose rows reads a
-        // page skips its exponentials (P = 0 there)
-        mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
-        wm[k] = __any_sync(0xffffffffu, mem[k]);
-        wany |= wm[k];
-      }
-      uint32_t pk[kSCols / 2];
-#pragma unroll
-      for (int i = 0; i < kSCols / 2; ++i) pk[i] = 0u;
-      if (wany) {
-        float v[kSCols];
-        {
-          // only the pages this warp's rows read: TMEM read bandwidth is a
-          // shared per-SM resource (a private page is read by one warp)
-          uint32_t sr[kSCols];
-#ifdef TTS_LD32
-          tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
-          tc_wait_ld();
-#pragma unroll
-          for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
-#else
-          if (wm[0] && wm[1]) {
-            tc_ld32(t_s + lane_off + (j & 1) * kSCols, sr);
-            tc_wait_ld();
-#pragma unroll
-            for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
-          } else {
-            // one page: 16 columns
-            const int k1 = wm[0] ? 0 : 1;
-            tc_ld16(t_s + lane_off + (j & 1) * kSCols + k1 * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
-            tc_wait_ld();
-#pragma unroll
-            for (int i = 0; i < kP; ++i) {
-              v[i] = k1 == 0 ? __uint_as_float(sr[i]) : -INFINITY;
-              v[kP + i] = k1 == 1 ? __uint_as_float(sr[i]) : -INFINITY;
-            }
-          }
-#endif
-        }
-        // raw scores (scale > 0 commutes with max); rows not reading page k
-        // are masked once per page (max -> -inf, exponent offset -> -inf, so
-        // P is exactly 0); token slots >= ntok only on a partial page
-        float mx = -INFINITY;
+    if (n_pieces > 0 && n1 == 0) {  // first piece in phase 2: Q after the plan
+      int gi, slab, j0, j1, pslot;
+      piece(0, gi, slab, j0, j1, pslot);
+      load_q(gi, slab);
+    }
+    int js = 0;
+    for (int pc = 0; pc < n_pieces; ++pc) {
+      int gi, slab, j0, j1, pslot;
+      piece(pc, gi, slab, j0, j1, pslot);
+      const GroupDesc g = group_of(gi);
+      int rbl = 0, rh = 0;
+      const bool rvalid = row_of(g, r, rbl, rh);
+      const int lrel = slab / p.Hkv, kh = slab % p.Hkv;
+      float m_ref = -1e30f, l = 0.f;
+      for (int j = j0; j < j1; ++j, ++js) {
+        if (r == 0) TTS_TR(js, 4);
+        bar_wait(b_sfull + 8 * (js & 1), (js >> 1) & 1u);
+        if (r == 0) TTS_TR(js, 5);
+        tc_fence_after();
+        const int slot = js % kNS;
+        int4 mt[kU];
+        bool mem[kU], wm[kU];
+        bool wany = false;
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
-          if (mt[k].x >= 0 && mt[k].z < kP) {
-#pragma unroll
-            for (int c = 0; c < kP; ++c)
-              if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
-          }
-          const float* w = v + k * kP;
-          float mk = fmax3(w[0], w[1], w[2]);
-#pragma unroll
-          for (int c = 3; c + 1 < kP; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
-          mk = fmaxf(mk, w[kP - 1]);
-          mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
+          mt[k] = meta[slot * kU + k];
+          // warp-uniform page membership: a warp none of whose rows reads a
+          // page skips its exponentials (P = 0 there)
+          mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
+          wm[k] = __any_sync(0xffffffffu, mem[k]);
+          wany |= wm[k];
         }
-        mx *= p.scale_log2;
-        const bool need = mx > m_ref + 8.0f;
-        if (__any_sync(0xffffffffu, need) && j > 0) {
-          if (r == 0) TTS_TR2(j, 7);
-          // every earlier PV product must have landed before O is rescaled in TMEM
-          bar_wait(b_pv + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1u);
-          tc_fence_after();
-          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
-#pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t o[32];
-            tc_ld32(t_o + lane_off + ch * 32, o);
-            tc_wait_ld();
+        uint32_t pk[kSCols / 2];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tc_st32(t_o + lane_off + ch * 32, o);
-          }
-          tc_wait_st();
-          l *= alpha;
-        }
-        if (need) m_ref = mx;
-        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-        float2 lacc = make_float2(0.f, 0.f);
+        for (int i = 0; i < kSCols / 2; ++i) pk[i] = 0u;
+        if (wany) {
+          float v[kSCols];
+          {
+            // only the pages this warp's rows read: TMEM read bandwidth is a
+            // shared per-SM resource (a private page is read by one warp)
+            uint32_t sr[kSCols];
+            if (wm[0] && wm[1]) {
+              tc_ld32(t_s + lane_off + (js & 1) * kSCols, sr);
+              tc_wait_ld();
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          if (wm[k]) {
-            const float nm = mem[k] ? -m_ref : -INFINITY;
-            const float2 nm2 = make_float2(nm, nm);
+              for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
+            } else {
+              const int pg = wm[0] ? 0 : 1;
+              tc_ld16(t_s + lane_off + (js & 1) * kSCols + pg * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
+              tc_wait_ld();
 #pragma unroll
-            for (int c = 0; c < kP; c += 2) {
-              const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
-              float a, b;
-              if (kPoly && ((c >> 1) & 1)) {
-                const float2 e2 = ex2_poly2(x);
-                a = e2.x;
-                b = e2.y;
-              } else {
-                a = ex2(x.x);
-                b = ex2(x.y);
+              for (int i = 0; i < kP; ++i) {
+                v[i] = pg == 0 ? __uint_as_float(sr[i]) : -INFINITY;
+                v[kP + i] = pg == 1 ? __uint_as_float(sr[i]) : -INFINITY;
               }
-              lacc = fadd2(lacc, make_float2(a, b));
-              pk[(k * kP + c) / 2] = pack_f16x2(a, b);
             }
           }
+          // raw scores (scale > 0 commutes with max); rows not reading page k
+          // are masked once per page (max -> -inf, exponent offset -> -inf, so
+          // P is exactly 0); token slots >= ntok only on a partial page
+          float mx = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < kU; ++k) {
+            if (mt[k].x >= 0 && mt[k].z < kP) {
+#pragma unroll
+              for (int c = 0; c < kP; ++c)
+                if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
+            }
+            const float* w = v + k * kP;
+            float mk = fmax3(w[0], w[1], w[2]);
+#pragma unroll
+            for (int c = 3; c + 1 < kP; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
+            mk = fmaxf(mk, w[kP - 1]);
+            mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
+          }
+          mx *= p.scale_log2;
+          const bool need = mx > m_ref + 8.0f;
+          if (__any_sync(0xffffffffu, need) && j > j0) {
+            if (r == 0) TTS_TR2(js, 7);
+            // every earlier PV product must have landed before O is rescaled in TMEM
+            bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
+            tc_fence_after();
+            const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+              uint32_t o[32];
+              tc_ld32(t_o + lane_off + ch * 32, o);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tc_st32(t_o + lane_off + ch * 32, o);
+            }
+            tc_wait_st();
+            l *= alpha;
+          }
+          if (need) m_ref = mx;
+          const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+          float2 lacc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < kU; ++k) {
+            if (wm[k]) {
+              const float nm = mem[k] ? -m_ref : -INFINITY;
+              const float2 nm2 = make_float2(nm, nm);
+#pragma unroll
+              for (int c = 0; c < kP; c += 2) {
+                const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
+                float a, b;
+                if (kPoly && ((c >> 1) & 1)) {
+                  const float2 e2 = ex2_poly2(x);
+                  a = e2.x;
+                  b = e2.y;
+                } else {
+                  a = ex2(x.x);
+                  b = ex2(x.y);
+                }
+                lacc = fadd2(lacc, make_float2(a, b));
+                pk[(k * kP + c) / 2] = pack_f16x2(a, b);
+              }
+            }
+          }
+          l += lacc.x + lacc.y;
         }
-        l += lacc.x + lacc.y;
+        // P (fp16) over the unit's first 16 S columns (value c at column c/2)
+        tc_st16(t_s + lane_off + (js & 1) * kSCols, pk);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (r == 0) TTS_TR(js, 6);
+        if (lane == 0) TTS_TR2(js, warp);
+        if (lane == 0) bar_arrive(b_pfull + 8 * (js & 1));
       }
-      // P (fp16) over the unit's first 16 S columns (value c at column c/2)
-      tc_st16(t_s + lane_off + (j & 1) * kSCols, pk);
-      tc_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (r == 0) TTS_TR(j, 6);
-      if (lane == 0) TTS_TR2(j, warp);
-      if (lane == 0) bar_arrive(b_pfull + 8 * (j & 1));
-    }
-    const int n_done = j;
-    // ---------------- epilogue ----------------
-    if (n_done > 0) {
-      bar_wait(b_pv + 8 * ((n_done - 1) & 1), ((n_done - 1) >> 1) & 1u);
+      // the next piece's Q (every S MMA of this piece has completed), so that
+      // its S = Q K^T overlaps this piece's epilogue
+      if (pc + 1 < n_pieces) {
+        int gi2, slab2, j02, j12, ps2;
+        piece(pc + 1, gi2, slab2, j02, j12, ps2);
+        load_q(gi2, slab2);
+      }
+      // ---------------- epilogue of the piece ----------------
+      // (an empty piece -- a tile with no units, e.g. under a sticky error --
+      // writes nothing)
+      const int tu = s_pre[gi + 1] - s_pre[gi];
+      if (j1 > j0) {
+      bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
       tc_fence_after();
-    }
-    if (p.splits == 1) {
-      if (n_done > 0) {
+      float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD;
+      if (j0 == 0 && j1 == tu) {
         const float inv = 1.f / l;
-        float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq +
-                               kh * G + rh) * kD;
 #pragma unroll 1
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t o[32];
@@ -693,93 +792,131 @@ __global__ void __launch_bounds__(kThreads, 2)
                               __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
           }
         }
-      }
-    } else {
-      // this slice's state (m, l, unnormalised O) -> smem for the cluster merge
-      float* op = reinterpret_cast<float*>(bp + kOffRing);  // the ring is idle now
-      m_s[r] = m_ref;
-      l_s[r] = l;
+      } else {
+        // a5: this piece's (m, l, unnormalised O) -> its partial slot (2c for the
+        // CTA's first phase-2 piece, 2c + 1 for its last); O stored chunk-major
+        // ([32 chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
+        // The last piece to finish merges.
+        float* part = p.partial + (size_t)pslot * kPartFloats;
+        part[r] = m_ref;
+        part[kRows + r] = l;
+        float4* po = reinterpret_cast<float4*>(part + 2 * kRows) + r;
 #pragma unroll 1
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t o[32];
-        if (n_done > 0) {
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t o[32];
           tc_ld32(t_o + lane_off + ch * 32, o);
           tc_wait_ld();
-        } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = 0u;
+          for (int i = 0; i < 8; ++i)
+            __stcg(po + (ch * 8 + i) * kRows,
+                   make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
+                               __uint_as_float(o[4 * i + 3])));
         }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int64_t T0 = F(slab * ng + gi);
+        auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
+          if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
+          int lo = 0, hi = C2;  // largest c with start2(c) <= x
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (start2(mid) <= x) lo = mid;
+            else hi = mid;
+          }
+          return lo;
+        };
+        const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
+        const int tile = slab * ng + gi;
+        if (r == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_info[0]) {
+          __threadfence();
+          const int np = c_last - c_first + 1;
+          // piece k's slot: only the first CTA's range can start before the tile
+          const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
+          auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
+          // latency-bound (L2 round trips under full HBM load): every batch of
+          // loads is issued before any is consumed
+          float M = -INFINITY, L = 0.f;
+          for (int k0 = 0; k0 < np; k0 += 8) {
+            float mv[8], lv[8];
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) {
-          const int c = ch * 8 + q4;  // 16-B chunk of the row, XOR-swizzled against bank conflicts
-          *reinterpret_cast<float4*>(op + r * kD + ((c & ~7) | ((c & 7) ^ (r & 7))) * 4) =
-              make_float4(__uint_as_float(o[4 * q4]), __uint_as_float(o[4 * q4 + 1]),
-                          __uint_as_float(o[4 * q4 + 2]), __uint_as_float(o[4 * q4 + 3]));
+            for (int i = 0; i < 8; ++i) {
+              const bool ok = k0 + i < np;
+              mv[i] = ok ? __ldcg(part_of(k0 + i) + r) : -INFINITY;
+              lv[i] = ok ? __ldcg(part_of(k0 + i) + kRows + r) : 0.f;
+            }
+            float M2 = M;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) M2 = fmaxf(M2, mv[i]);
+            L *= exp2f(M - M2);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) L += k0 + i < np ? exp2f(mv[i] - M2) * lv[i] : 0.f;
+            M = M2;
+          }
+          const float inv = 1.f / L;
+#pragma unroll 1
+          for (int ch = 0; ch < 4; ++ch) {
+            float4 acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < np; k += 2) {
+              const bool two = k + 1 < np;
+              const float* pa = part_of(k);
+              const float* pb = part_of(two ? k + 1 : k);
+              const float wa = __ldcg(pa + r), wb = __ldcg(pb + r);
+              const float4* sa = reinterpret_cast<const float4*>(pa + 2 * kRows) + r;
+              const float4* sb = reinterpret_cast<const float4*>(pb + 2 * kRows) + r;
+              float4 xa[8], xb[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                xa[i] = __ldcg(sa + (ch * 8 + i) * kRows);
+                xb[i] = __ldcg(sb + (ch * 8 + i) * kRows);
+              }
+              const float fa = exp2f(wa - M), fb = two ? exp2f(wb - M) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                acc[i].x += fa * xa[i].x + fb * xb[i].x;
+                acc[i].y += fa * xa[i].y + fb * xb[i].y;
+                acc[i].z += fa * xa[i].z + fb * xb[i].z;
+                acc[i].w += fa * xa[i].w + fb * xb[i].w;
+              }
+            }
+            if (rvalid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                *reinterpret_cast<float4*>(orow + ch * 32 + 4 * i) =
+                    make_float4(acc[i].x * inv, acc[i].y * inv, acc[i].z * inv, acc[i].w * inv);
+            }
+          }
+          if (r == 0) p.tile_cnt[tile] = 0;  // every piece of the tile has arrived: ready for the next call
         }
       }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) bar_arrive(b_ofree);  // the next piece's first PV may overwrite O
     }
   }
 
   if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
   if (threadIdx.x == 0) TTS_CTA(1, gtimer());
-  if (p.splits > 1) {
-    // a5: the S slices' partial states of every row merged through DSMEM;
-    // this CTA merges rows [split * 128 / S, (split + 1) * 128 / S)
-    cluster_sync();
-    if (warp < 4) {
-      const int S = p.splits;
-      const int rpc = kRows / S;
-      const int tpr = 128 / rpc;
-      const int row = split * rpc + threadIdx.x / tpr;
-      const int cseg = threadIdx.x % tpr;
-      const int cw = kD / tpr;
-      int bl = 0, hd = 0;
-      const bool ok = row_of(row, bl, hd) && !*s_bail;
-      const uint32_t lm = su32(m_s + row), ll = su32(l_s + row);
-      // all remote loads of a step are issued before any is consumed (DSMEM
-      // latency ~200 cycles; dependent loads would serialise)
-      float mk[8], lk[8], wk[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        mk[k] = k < S ? ld_dsmem_f32(mapa(lm, k)) : -INFINITY;
-        lk[k] = k < S ? ld_dsmem_f32(mapa(ll, k)) : 0.f;
-      }
-      float M = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) M = fmaxf(M, mk[k]);
-      float L = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        wk[k] = k < S ? exp2f(mk[k] - M) : 0.f;
-        L += wk[k] * lk[k];
-      }
-      const float inv = 1.f / L;
-      float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + bl) * p.Hq +
-                             kh * G + hd) * kD;
-      for (int c4 = 0; c4 < cw / 4; ++c4) {
-        const int c = cseg * (cw / 4) + c4;
-        const int pc = (c & ~7) | ((c & 7) ^ (row & 7));
-        const uint32_t la = base + kOffRing + (uint32_t)(row * kD + pc * 4) * 4;
-        float4 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = k < S ? ld_dsmem_f32x4(mapa(la, k)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          acc.x += wk[k] * v[k].x;
-          acc.y += wk[k] * v[k].y;
-          acc.z += wk[k] * v[k].z;
-          acc.w += wk[k] * v[k].w;
-        }
-        if (ok) *reinterpret_cast<float4*>(orow + c * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-      }
-    }
-    cluster_sync();
-  }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
   if (threadIdx.x == 0) TTS_CTA(2, gtimer());
+#ifdef TTS_TRACE
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    long long units = ub2 - ua2;
+    for (int k = 0; k < n1; ++k) {
+      const int t = blockIdx.x + k * Cg, gi = t % ng;
+      units += s_pre[gi + 1] - s_pre[gi];
+    }
+    TTS_CTA(3, units | ((long long)smid << 32));
+  }
+#endif
   if (warp == 5) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -796,6 +933,9 @@ extern "C" int tts_debug_read_trace(long long* out_h) {
 }
 #endif
 
+size_t umma_partial_bytes() { return (size_t)2 * kMaxCtas * kPartFloats * 4; }
+int umma_max_groups() { return kMaxGroups; }
+
 bool umma_supported(const Ctx* c) {
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
   return c->cfg.head_dim == kD && c->cfg.page_size == kP && G >= 4 && G <= 16 && c->tmap3_ok && c->tmap_ok;
@@ -808,7 +948,7 @@ int umma_max_beams(const Ctx* c) {
 }
 
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
-                                  int n_lens, int splits, int layer_begin, int n_layers, int n_call,
+                                  int n_lens, int layer_begin, int n_layers, int n_call,
                                   const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
                                   const __nv_bfloat16* v_new, cudaStream_t st) {
   PlanParams pp;
@@ -847,7 +987,10 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.G = p.Hq / p.Hkv;
   p.maxB = c->cfg.max_beams;
   p.maxP = c->cfg.max_pages_per_beam;
-  p.splits = splits;
+  p.n_layers = n_layers;
+  p.n_groups = n_groups;
+  p.partial = c->ws_partial;
+  p.tile_cnt = c->ws_tile_cnt;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
   UInline inl;  // host staging of the parameter block (copied by the launch)
@@ -895,18 +1038,13 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_groups * splits, p.Hkv, n_layers);
+  // persistent: two CTAs per SM (the smem / TMEM / register budget of one CTA)
+  cfg.gridDim = dim3(std::min(2 * c->num_sms, kMaxCtas));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = splits;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1] = pdl;
-  cfg.attrs = attr;
-  cfg.numAttrs = no_pdl ? 1 : 2;
+  cfg.attrs = &pdl;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, c->tmap_k, c->tmap3_v, p, inl);
   c->launches++;
   return e;

@@ -86,6 +86,8 @@ struct Ctx {
   int4* ws_items = nullptr;      // [2][max_requests * max_beams * max_pages_per_beam]
   int32_t* ws_counts = nullptr;  // [2][max_requests * max_beams]
   int plan_parity = 0;
+  float* ws_partial = nullptr;     // split tiles' partial (m, l, O) (attention_umma.cu)
+  int32_t* ws_tile_cnt = nullptr;  // [num_layers * num_kv_heads * max groups], zero between launches
 };
 
 // ---- pool value format --------------------------------------------------------
@@ -156,8 +158,10 @@ int umma_max_beams(const Ctx* c);
 // + a3 (plan, built on the fly per CTA) + a4.  groups_h / lens_h are HOST
 // arrays (group descriptors; per group-beam post-append lengths, 0 = inactive,
 // GroupDesc.pad[0] = offset), sent in the kernel parameter block when they fit.
+size_t umma_partial_bytes();
+int umma_max_groups();
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
-                                  int n_lens, int splits, int layer_begin, int n_layers, int n_call,
+                                  int n_lens, int layer_begin, int n_layers, int n_call,
                                   const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
                                   const __nv_bfloat16* v_new, cudaStream_t s);
 
