@@ -2,34 +2,32 @@
 // (tcgen05 + TMEM + TMA), sm_100a.  Same contract as attention.cu (see there
 // and include/tts.h); this is the path for head_dim 128 and 4 <= G <= 16.
 //
-// One launch per call (k_tree_umma).  Per CTA, before the tile loop:
-// a2 (tts_decode_step): the call's new token of each active beam of the group,
-// for this CTA's (layer, kv head), is written into the beam's last page (V
-// converted to the pool's fp16; a fresh page's other slots zeroed).  The last
-// page of a beam is private to it (eager copy-on-write), so no other CTA reads
-// what this CTA writes.
-// a3 (plan): the ordered list of DISTINCT pages of the group's block-table rows
-// -- a run of <= floor(128/G) consecutive beams of one request in DFS order, so
-// that every shared page's beams are adjacent (ledger C5) --
-// each with its member-beam bitmask and valid-token count, built on the fly by
-// the producer warp 32 positions at a time (lane = position) and fed straight
-// into the TMA ring.
-// a4: one CTA owns a 128-row query tile (the group's beams x the
-// G query heads of one kv head) for one layer, and a contiguous, balanced
-// slice of the group's page list when the grid would not fill the GPU.
+// Two launches per call, chained by programmatic dependent launch:
+// k_plan      a2 (tts_decode_step): the call's new token of each active beam
+//             -> slot (len-1) % P of the beam's last page (V converted to the
+//             pool's fp16; a fresh page's other slots zeroed).  The last page
+//             of a beam is private to it (eager copy-on-write).
+//             a3 (plan): per beam group -- a run of consecutive beams of one
+//             request in DFS order, so that every shared page's beams are
+//             adjacent (ledger C5) -- the ordered list of its
+//             DISTINCT pages, each with its member-beam bitmask and valid-token
+//             count.
+// k_tree_umma a4 (+ a5): persistent, 2 CTAs per SM.  A tile is (group, kv
+//             head, layer): the group's beams x the G query heads of the kv
+//             head, <= 128 rows, against the group's page list.  Whole tiles
+//             round-robin first, then the rest split over all CTAs (stream-K)
+//             and merged through a global partial buffer.
 // Per unit of two pages:
-//   producer warp  TMA (3D box = one 16x128 bf16 tile, SWIZZLE_128B) -> smem ring
-//   MMA warp       S[128 x 32] = Q . K^T     tcgen05.mma kind::f16, S in TMEM
-//   softmax WG     one thread per row: tcgen05.ld S; mask rows whose beam does not
-//                  reference the page and token slots >= ntok; fp32 online softmax
-//                  with lazy rescale (O rescaled in TMEM only when the running max
-//                  grows by > 2^8); P in fp16 -> tcgen05.st over S
-//   MMA warp       O[128 x 128] += P . V   fp16 x fp16 (A from TMEM; V is kept in
-//                  fp16 in the pool, MN-major operand; ledger C14)
-// Each distinct page is fetched once per CTA and multiplied against all 128
+//   producer warp   TMA (16x128 bf16 K / fp16 V tiles, SWIZZLE_128B) -> smem ring
+//   S warp          S[128 x 32] = Q . K^T     tcgen05.mma kind::f16, S in TMEM
+//   softmax warps   one thread per row: tcgen05.ld S; mask rows whose beam does not
+//                   reference the page and token slots >= ntok; fp32 online softmax
+//                   with lazy rescale (O rescaled in TMEM only when the running max
+//                   grows by > 2^8); P in fp16 -> tcgen05.st over S
+//   PV warp         O[128 x 128] += P . V   fp16 x fp16 (A from TMEM; V is kept in
+//                   fp16 in the pool, MN-major operand; ledger C14)
+// Each distinct page is fetched once per tile and multiplied against all its
 // rows: every GQA head and every beam of the tile that references it.
-// Slices of one tile form a thread-block cluster; their partial (m, l, O) are
-// merged through distributed shared memory, never through HBM.
 #include <cstdlib>
 #include <cstring>
 

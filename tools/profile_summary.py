@@ -35,7 +35,7 @@ for r in rows:
     d = dict(zip(hdr, r))
     if d.get("Metric Name") != "gpu__time_duration.sum":
         continue
-    name = d["Kernel Name"].split("(")[0].replace("tts::<unnamed>::", "")
+    name = d["Kernel Name"].split("(")[0].replace("tts::<unnamed>::", "").replace("void ", "")
     unit = d.get("Metric Unit", "ns")
     v = float(d["Metric Value"].replace(",", ""))
     v = v * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1e-3)
@@ -62,6 +62,7 @@ dram_r = val("dram__bytes_read.sum")
 dram_w = val("dram__bytes_write.sum")
 dur_us = val("gpu__time_duration.sum")
 cb = json.load(open(cbytes))
+skip = skip % len(cb["unique_kv_bytes"])  # the captured launch's index within one bench step
 algo_kv = cb["unique_kv_bytes"][skip]
 algo = algo_kv + cb["active_beams"][skip] * cb["qo_bytes_per_beam"]
 keys = ["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
