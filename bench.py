@@ -456,9 +456,14 @@ def main():
         b = SpanBench(cfg, ws, rank, local)
         greqs = [0]
     elif cfg.step_len == 0:
-        # straggler batch: shard the R requests over ranks (request r -> rank r mod G)
+        # straggler batch: shard the R requests over ranks (request r -> rank r mod G).
+        # The 64-request batch is defined for 2/4/8 GPUs; its page pool does not
+        # fit one GPU (64 x 6000 pages x 459 KB), so N = 1 runs the 4-GPU shard
+        # (16 requests) unless --requests says otherwise.
         if args.requests:
             cfg = cfg.with_(R=args.requests)
+        elif ws == 1:
+            cfg = cfg.with_(R=16)
         greqs = [r for r in range(cfg.R) if r % ws == rank]
         scaling = "strong"
         # page budget: runner.pages_per_request (override with --pages-per-request)
