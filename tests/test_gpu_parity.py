@@ -123,3 +123,29 @@ def test_out_of_pages_sticky_status():
     q, k, v = r.inputs.step(0, [0])
     r.ctx.tts_block_table_append([0], None, k, v)
     assert r.ctx.tts_device_status() == 3  # TTS_ERR_OUT_OF_PAGES
+
+
+@pytest.mark.parametrize("name,cfg", [
+    # 4 tiles over 296 CTAs: every tile split ~74 ways (phase-2 stream-K, merge of > 8 pieces)
+    ("split", workload.Config("split", R=1, N=16, M=4, L=2, Hq=12, Hkv=2, d=128, P=16, prompt=256,
+                              n_steps=3, step_len=64, seed=4242)),
+    # C3-like: one round of whole tiles + a stream-K remainder (448 tiles)
+    ("hybrid", workload.C3.with_(n_steps=2, step_len=32)),
+])
+def test_outputs_bit_identical_across_runs(name, cfg):
+    """The split-tile merge reads the pieces in a fixed order, so repeated runs
+    give bit-identical outputs whatever the order in which CTAs finish
+    (SURVEY 8(b) "Determinism")."""
+    from paper_2509_00195_b200.runner import BeamStepRunner
+
+    def run():
+        outs = []
+        r = BeamStepRunner(cfg)
+        r.run(on_iter=lambda it, out, active: outs.append(out.clone()))
+        r.release()
+        return outs
+
+    a, b = run(), run()
+    assert len(a) == len(b) > 0
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
