@@ -157,16 +157,22 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t ctx, int32_t layer_begin, int32_t 
                                     float softmax_scale, float* out, void* stream);
 
 /* a2+a4 fused: tts_block_table_append then tts_prefix_attn_decode over all
- * layers [0, L) in one call (one round of host planning, same kernels and
- * semantics as the two calls in sequence).  Shapes as in those calls. */
+ * layers [0, L) in one call (one round of host planning, same semantics as
+ * the two calls in sequence).  Shapes as in those calls.  On the tcgen05 path
+ * the call is k_alloc (only when a beam crosses a page boundary), k_plan
+ * (append + page-list plan) and the persistent attention kernel, chained by
+ * programmatic dependent launch; a call's k_plan may run while the previous
+ * call's attention kernel still runs (it writes nothing that kernel reads). */
 tts_status_t tts_decode_step(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
                              const uint8_t* active_h, const void* k_new, const void* v_new,
                              const void* q, float softmax_scale, float* out, void* stream);
 
 /* Live timing of the attention kernel: between tts_profile_begin and
- * tts_profile_end every attention launch is bracketed by CUDA events recorded
- * on its own stream; tts_profile_end syncs and returns the summed kernel time
- * (ms) and the number of attention launches. */
+ * tts_profile_end every attention launch (k_plan + attention kernel on the
+ * tcgen05 path) is bracketed by CUDA events recorded on its own stream;
+ * tts_profile_end syncs and returns the summed time (ms) and the number of
+ * attention launches.  The events serialise consecutive calls (bench.py times
+ * runs of calls between forks instead). */
 tts_status_t tts_profile_begin(tts_ctx_t ctx);
 tts_status_t tts_profile_end(tts_ctx_t ctx, double* attn_ms_h, int64_t* attn_launches_h);
 
