@@ -141,6 +141,37 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
+class H2DPipe:
+    """Double-buffered host -> device staging of each call's inputs on a copy
+    stream, so that the next call's q/k/v copy overlaps this call's kernels
+    (the way a serving loop feeds the C-ABI from pinned host memory)."""
+
+    def __init__(self, like, dev):
+        self.slots = [tuple(torch.empty_like(t) for t in like) for _ in range(2)]
+        self.cs = torch.cuda.Stream(dev)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        self.dev = dev
+
+    def stage(self, hq, hk, hv):
+        s = self.i & 1
+        with torch.cuda.stream(self.cs):
+            self.cs.wait_event(self.free[s])  # the call that last used this slot has run
+            q, k, v = self.slots[s]
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            self.ready[s].record(self.cs)
+        torch.cuda.current_stream(self.dev).wait_event(self.ready[s])
+        return q, k, v
+
+    def release(self):
+        self.free[self.i & 1].record(torch.cuda.current_stream(self.dev))
+        self.i += 1
+
+
+# ---------------------------------------------------------------------------
 class Bench:
     """Drives one rank's requests through libtts with minimal host overhead."""
 
@@ -217,32 +248,30 @@ class Bench:
             else:
                 if e2e is not None:
                     hq, hk, hv = e2e["ring"][it.t % nr]
-                    q = e2e["q"]
-                    k = e2e["k"]
-                    v = e2e["v"]
-                    q.copy_(hq, non_blocking=True)
-                    k.copy_(hk, non_blocking=True)
-                    v.copy_(hv, non_blocking=True)
                 if self.batched:
+                    if e2e is not None:
+                        q, k, v = e2e["pipe"].stage(hq, hk, hv)
                     loc = [self.local[r] for r in it.reqs]
                     arr = (ctypes.c_int32 * len(loc))(*loc)
                     act = np.ascontiguousarray(np.stack(it.active), dtype=np.uint8)
                     self._chk(lib.tts_decode_step(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
                                                   k.data_ptr(), v.data_ptr(), q.data_ptr(), self.scale,
                                                   self.out.data_ptr(), st), "decode_step")
+                    if e2e is not None:
+                        e2e["pipe"].release()
                     if stats_accum is not None:
                         self._chk(lib.tts_block_table_stats(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
                                                             stats_accum[self.ncall].data_ptr(), st), "stats")
                         self.ncall += 1
                 else:
                     for ri, r in enumerate(it.reqs):
-                        if e2e is not None and ri > 0:  # every call's q/k/v come from the host
-                            q.copy_(hq, non_blocking=True)
-                            k.copy_(hk, non_blocking=True)
-                            v.copy_(hv, non_blocking=True)
+                        if e2e is not None:  # every call's q/k/v come from the host
+                            q, k, v = e2e["pipe"].stage(hq, hk, hv)
                         arr = self.req_arr[self.local[r]]
                         self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
                                                       self.scale, self.out.data_ptr(), st), "decode_step")
+                        if e2e is not None:
+                            e2e["pipe"].release()
                         if stats_accum is not None:
                             self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum[self.ncall].data_ptr(),
                                                                 st), "stats")
@@ -337,12 +366,11 @@ class SpanBench:
                 open_ev.record(torch.cuda.current_stream(self.dev))
             if e2e is not None:
                 hq, hk, hv = e2e["ring"][it.t % nr]
-                q, k, v = e2e["q"], e2e["k"], e2e["v"]
-                q.copy_(hq, non_blocking=True)
-                k.copy_(hk, non_blocking=True)
-                v.copy_(hv, non_blocking=True)
+                q, k, v = e2e["pipe"].stage(hq, hk, hv)
             self._chk(lib.tts_decode_step(h, 1, self.req, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
                                           self.scale, self.out.data_ptr(), st), "decode_step")
+            if e2e is not None:
+                e2e["pipe"].release()
             if stats_accum is not None:
                 self._chk(lib.tts_block_table_stats(h, 1, self.req, None, stats_accum[self.ncall].data_ptr(), st),
                           "stats")
@@ -551,7 +579,7 @@ def main():
     if args.e2e_steps > 0:
         ring = [(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()) for q, k, v in b.ring]
         q0, k0, v0 = b.ring[0]
-        ctx_e = {"ring": ring, "q": torch.empty_like(q0), "k": torch.empty_like(k0), "v": torch.empty_like(v0),
+        ctx_e = {"ring": ring, "pipe": H2DPipe((q0, k0, v0), dev),
                  "d2h": 0, "parents": [], "last_out": torch.empty(b.out.shape, dtype=torch.float32).pin_memory()}
         h2d = sum(1 for it in b.sched for _ in (it.reqs if not b.batched else [0])) * \
             (q0.numel() * 2 + k0.numel() * 2 + v0.numel() * 2)
