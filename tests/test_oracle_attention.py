@@ -88,14 +88,75 @@ def test_split_merge_identity(seed):
     assert np.allclose(m, m1) and np.allclose(l, l1, rtol=1e-12)
 
 
-def test_oracle_run_c1_outputs_are_sdpa_of_gathered_pages():
-    """End to end on C1: the per-beam (list) attention equals SDPA over K/V
-    gathered through the block-table simulator's pages."""
-    cfg = workload.C1
+def _identity_kv(cfg, ident, l):
+    """K/V [n, Hkv, d] of a list of token identities, regenerated from synth by
+    the identity definitions of synth/rng.py (prompt token i of request r ->
+    *_PROMPT keyed (layer, r, i, kv head); the token beam slot b appended at
+    iteration t -> keyed (layer, r, t, b, kv head)).  Written here from those
+    definitions, not through oracle.run.KVSource."""
+    from synth import rng
+    kvh = torch.arange(cfg.Hkv).view(1, -1)
+    n = len(ident)
+    K = torch.empty(n, cfg.Hkv, cfg.d, dtype=torch.float64)
+    V = torch.empty_like(K)
+    ip = [k for k, tok in enumerate(ident) if tok[0] == "p"]
+    idd = [k for k, tok in enumerate(ident) if tok[0] == "d"]
+    if ip:
+        r = torch.tensor([ident[k][1] for k in ip]).view(-1, 1)
+        i = torch.tensor([ident[k][2] for k in ip]).view(-1, 1)
+        K[ip] = rng.kv_prompt_values(cfg.seed, "k", l, r, i, kvh, cfg.d).double()
+        V[ip] = rng.kv_prompt_values(cfg.seed, "v", l, r, i, kvh, cfg.d).double()
+    if idd:
+        r, t, b = (torch.tensor([ident[k][j] for k in idd]).view(-1, 1) for j in (1, 2, 3))
+        K[idd] = rng.kv_decode_values(cfg.seed, "k", l, r, t, b, kvh, cfg.d).double()
+        V[idd] = rng.kv_decode_values(cfg.seed, "v", l, r, t, b, kvh, cfg.d).double()
+    return K, V
+
+
+def _sdpa_default_scale(q, K, V, G):
+    """fp64 library SDPA at its DEFAULT scale (1/sqrt(d), ledger C10), GQA expanded."""
+    Hq, d = q.shape
+    tq = q.view(1, Hq, 1, d)
+    tk = K.permute(1, 0, 2).repeat_interleave(G, dim=0).unsqueeze(0)
+    tv = V.permute(1, 0, 2).repeat_interleave(G, dim=0).unsqueeze(0)
+    return torch.nn.functional.scaled_dot_product_attention(tq, tk, tv)[0, :, 0].numpy()
+
+
+@pytest.mark.parametrize("cfg", [
+    workload.C1,
+    # partial prompt page (37 tokens), straggler steps, G = 3, >= 2 forks
+    workload.Config("pin-rand", R=2, N=6, M=3, L=2, Hq=6, Hkv=2, d=32, P=16, prompt=37, n_steps=4,
+                    step_len=0, ln_mu=math.log(9), ln_sigma=0.8, ln_cap=30, seed=31337, q_scale=4.0),
+], ids=["C1", "rand-partial-prompt"])
+def test_oracle_beam_output_is_sdpa_over_block_table_gather(cfg):
+    """Pins OracleRun.beam_output (ledger C10 scale 1/sqrt(d), C11 the new token
+    attends to itself, and which tokens make up a beam's context) against an
+    independent definition: the beam's token identities read through the
+    block-table simulator's pages (BlockTableSim.gather),
+    K/V/q regenerated from those identities, fp64 SDPA at its default scale.
+    The query of beam b at iteration t is keyed (layer, r, t, b, q head); the
+    token it attends to last is the one it appended at t (PAPER.md P:338,
+    GenerateOneToken precedes the step's attention; P:148 paged attention)."""
+    from synth import rng
     run = OracleRun(cfg)
-    tr = run.run(sample=lambda it: [(r, b, 0) for r in it.reqs for b in range(cfg.N) if it.t % 7 == 0])
-    assert tr.beam_steps == cfg.N * cfg.n_steps * cfg.step_len
-    assert len(tr.forks) == cfg.n_steps - 1
-    assert len(tr.outputs) > 0
+    gathered = {}
+
+    def sample(it):
+        pts = []
+        for k, r in enumerate(it.reqs):
+            for b in range(cfg.N):
+                if it.active[k][b] and (it.t % 3 == 0 or it.forks):
+                    gathered[(it.t, r, b)] = run.sim.gather(r, b)
+                    pts += [(r, b, l) for l in range(cfg.L)]
+        return pts
+
+    tr = run.run(sample=sample)
+    assert len(tr.forks) >= 2 and len(tr.outputs) > 0
+    hq = torch.arange(cfg.Hq)
     for (t, r, b, l), o in tr.outputs.items():
-        assert o.shape == (cfg.Hq, cfg.d) and np.isfinite(o).all()
+        ident = gathered[(t, r, b)]
+        assert ident[-1] == ("d", r, t, b)  # the token appended at t is the last one attended
+        K, V = _identity_kv(cfg, ident, l)
+        q = rng.q_values(cfg.seed, l, r, t, b, hq, cfg.d, cfg.q_scale).double()
+        ref = _sdpa_default_scale(q, K, V, cfg.G)
+        assert np.abs(o - ref).max() <= 1e-12, (t, r, b, l)
