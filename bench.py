@@ -6,13 +6,18 @@ request a rank holds: install on the prompt, every decode iteration (append +
 prefix-shared attention over all L layers), a select + fork after every TTS
 step but the last, release.  All SURVEY 8(a) rows are inside the timed region.
 
-Workload (BASELINE.json configs): default C2 (configs[1], Qwen2.5-Math-1.5B
-attention shape, N=16, M=4, 2k-token chains).  L2 control: each rank rotates
---rotate independent requests of that shape, one request per C-ABI call, so
-the reuse distance of any KV page between two positions is >= 2x the 126 MB
-L2 (SURVEY 8(d) pitfall 1: "rotate across independent request pools").
-Multi-GPU: one process per GPU, each with its own requests (no collective on
-the data path; SURVEY 8(e) C4 partitioning) -> "scaling": "weak".
+Workload (BASELINE.json configs; the metric names none, so N = 1 runs the
+largest single-GPU configuration): default at N = 1 is C3 (configs[2],
+Qwen2.5-Math-7B attention shape, N = 64, M = 4, 4k-token chains; its unique KV
+per position, ~1.4 GB, is >> the 126 MB L2, so consecutive calls find nothing
+of theirs in L2 -- SURVEY 8(d) pitfall 1 "inputs larger than L2").  C2 and the
+other configs via --config; C2 rotates --rotate independent requests (one per
+call) so that the reuse distance of a page spans >= 2x L2.
+Multi-GPU: one process per GPU.  Default at N > 1 is C4 (64 concurrent
+requests, request r -> rank r mod N, no data-path collective, "scaling":
+"strong"); --config C5 spreads one request's 512 beams over the ranks (NCCL
+all-gather of scores + lineage migration per step).  `--gpus N` without
+torchrun re-launches itself under torch.distributed.run with N processes.
 
 --impl reference times the CPU oracle (the only reference this paper-only
 task has) on the host cores, on a bounded sample of the same workload.
@@ -24,6 +29,7 @@ import ctypes
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,7 +45,8 @@ from synth import workload  # noqa: E402
 
 METRIC = "beam-steps/s and HBM GB/s (unique KV) vs roofline at 1/2/4/8 B200"
 UNIT = "beam-steps/s"
-DEFAULT_ROTATE = {"C1": 64, "C2": 32, "C3": 4, "C4": 1, "C5": 1}
+DEFAULT_ROTATE = {"C1": 64, "C2": 32, "C3": 1, "C4": 1, "C5": 1}
+HBM_SPEC_GBS = 8000.0  # north_star "~8 TB/s"
 
 
 def parse():
@@ -48,11 +55,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="libtts", choices=["libtts", "reference"])
-    ap.add_argument("--config", default="C2", choices=list(workload.CONFIGS))
+    ap.add_argument("--config", default=None, choices=list(workload.CONFIGS),
+                    help="default: C3 at N = 1, C4 at N > 1")
     ap.add_argument("--rotate", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=18.0)
     ap.add_argument("--dump-call-bytes", default="")
     ap.add_argument("--requests", type=int, default=0, help="override R of the straggler batch (C4)")
     ap.add_argument("--tts-steps", type=int, default=0, help="override the number of TTS steps (shorter chains)")
@@ -61,10 +69,37 @@ def parse():
     return ap.parse_args()
 
 
+def resolve_config(args, ws):
+    return args.config or ("C3" if ws == 1 else "C4")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """`--gpus N` (N > 1) outside torchrun: re-launch under torch.distributed.run,
+    one process per GPU; fail loudly if the box has fewer GPUs."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if args.impl == "libtts":
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}\n")
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_init(n):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws != n:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {n}")
     if ws > 1:
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
@@ -141,34 +176,52 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-class H2DPipe:
-    """Double-buffered host -> device staging of each call's inputs on a copy
-    stream, so that the next call's q/k/v copy overlaps this call's kernels
-    (the way a serving loop feeds the C-ABI from pinned host memory)."""
+class IOPipe:
+    """Host <-> device traffic of a serving loop that feeds the C-ABI from host
+    buffers: each call's q/k/v are copied H2D (pinned, on a copy stream) into
+    one of two device slots while the previous call computes, and each call's
+    output is copied D2H (pinned, on a second copy stream) once the call has
+    run, so the next call's kernels overlap both copies."""
 
-    def __init__(self, like, dev):
-        self.slots = [tuple(torch.empty_like(t) for t in like) for _ in range(2)]
-        self.cs = torch.cuda.Stream(dev)
+    def __init__(self, like_in, like_out, dev):
+        self.slots = [tuple(torch.empty_like(t) for t in like_in) for _ in range(2)]
+        self.outs = [torch.empty_like(like_out) for _ in range(2)]
+        self.host_out = [torch.empty(like_out.shape, dtype=like_out.dtype).pin_memory() for _ in range(2)]
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
         self.ready = [torch.cuda.Event() for _ in range(2)]
-        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.used = [torch.cuda.Event() for _ in range(2)]
+        self.out_free = [torch.cuda.Event() for _ in range(2)]
         self.i = 0
         self.dev = dev
+        self.d2h_bytes = 0
 
     def stage(self, hq, hk, hv):
         s = self.i & 1
-        with torch.cuda.stream(self.cs):
-            self.cs.wait_event(self.free[s])  # the call that last used this slot has run
+        with torch.cuda.stream(self.h2d):
+            self.h2d.wait_event(self.used[s])  # the call that last read this slot has run
             q, k, v = self.slots[s]
             q.copy_(hq, non_blocking=True)
             k.copy_(hk, non_blocking=True)
             v.copy_(hv, non_blocking=True)
-            self.ready[s].record(self.cs)
-        torch.cuda.current_stream(self.dev).wait_event(self.ready[s])
-        return q, k, v
+            self.ready[s].record(self.h2d)
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_event(self.ready[s])
+        cur.wait_event(self.out_free[s])  # this slot's previous output has reached the host
+        return q, k, v, self.outs[s]
 
     def release(self):
-        self.free[self.i & 1].record(torch.cuda.current_stream(self.dev))
+        s = self.i & 1
+        self.used[s].record(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.used[s])
+            self.host_out[s].copy_(self.outs[s], non_blocking=True)
+            self.out_free[s].record(self.d2h)
+        self.d2h_bytes += self.outs[s].numel() * self.outs[s].element_size()
         self.i += 1
+
+    def drain(self):
+        torch.cuda.current_stream(self.dev).wait_stream(self.d2h)
 
 
 # ---------------------------------------------------------------------------
@@ -217,13 +270,16 @@ class Bench:
             from paper_2509_00195_b200.tts import TTSError
             raise TTSError(code, what)
 
-    def run_step(self, stats_accum=None, e2e=None, seg=None):
-        """One full run of every request.  e2e: dict of pinned host rings to copy from.
-        seg: list receiving one CUDA event pair (on the launching stream) per run of
-        consecutive decode calls between two forks (install / release excluded)."""
+    def run_step(self, stats_accum=None, e2e=None, seg=None, forks=None):
+        """One full run of every request.  e2e: dict with the pinned host input
+        ring and the IOPipe.  seg: list receiving one CUDA event pair (on the
+        launching stream) per run of consecutive decode calls between two forks
+        (install / release excluded).  forks: list receiving one event pair
+        around every tts_beam_select_fork call."""
         c = self.cfg
         open_ev = None
         lib, h, st = self.lib, self.h, self.stream
+        cur = torch.cuda.current_stream(self.dev)
         for r in self.greqs:
             k, v = self.prompt[self.local[r]]
             self._chk(lib.tts_block_table_init_request(h, self.local[r], c.N, c.prompt, k.data_ptr(),
@@ -235,9 +291,10 @@ class Bench:
         decode = lib.tts_decode_step
         for it in self.sched:
             q, k, v = self.ring[it.t % nr]
+            out = self.out
             if seg is not None and open_ev is None:
                 open_ev = torch.cuda.Event(enable_timing=True)
-                open_ev.record(torch.cuda.current_stream(self.dev))
+                open_ev.record(cur)
             if e2e is None and not self.batched and stats_accum is None:
                 # hot loop: one C-ABI call per request and position, arguments pre-marshalled
                 qp, kp, vp = ptrs[it.t % nr]
@@ -250,13 +307,13 @@ class Bench:
                     hq, hk, hv = e2e["ring"][it.t % nr]
                 if self.batched:
                     if e2e is not None:
-                        q, k, v = e2e["pipe"].stage(hq, hk, hv)
+                        q, k, v, out = e2e["pipe"].stage(hq, hk, hv)
                     loc = [self.local[r] for r in it.reqs]
                     arr = (ctypes.c_int32 * len(loc))(*loc)
                     act = np.ascontiguousarray(np.stack(it.active), dtype=np.uint8)
                     self._chk(lib.tts_decode_step(h, len(loc), arr, act.ctypes.data_as(ctypes.c_void_p),
                                                   k.data_ptr(), v.data_ptr(), q.data_ptr(), self.scale,
-                                                  self.out.data_ptr(), st), "decode_step")
+                                                  out.data_ptr(), st), "decode_step")
                     if e2e is not None:
                         e2e["pipe"].release()
                     if stats_accum is not None:
@@ -265,11 +322,11 @@ class Bench:
                         self.ncall += 1
                 else:
                     for ri, r in enumerate(it.reqs):
-                        if e2e is not None:  # every call's q/k/v come from the host
-                            q, k, v = e2e["pipe"].stage(hq, hk, hv)
+                        if e2e is not None:  # every call's q/k/v come from the host, its output goes back
+                            q, k, v, out = e2e["pipe"].stage(hq, hk, hv)
                         arr = self.req_arr[self.local[r]]
                         self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
-                                                      self.scale, self.out.data_ptr(), st), "decode_step")
+                                                      self.scale, out.data_ptr(), st), "decode_step")
                         if e2e is not None:
                             e2e["pipe"].release()
                         if stats_accum is not None:
@@ -279,7 +336,7 @@ class Bench:
             if it.forks or (seg is not None and it is self.sched[-1]):
                 if seg is not None:
                     e_end = torch.cuda.Event(enable_timing=True)
-                    e_end.record(torch.cuda.current_stream(self.dev))
+                    e_end.record(cur)
                     seg.append((open_ev, e_end))
                     open_ev = None
             if it.forks:
@@ -287,16 +344,23 @@ class Bench:
                 arr = (ctypes.c_int32 * len(loc))(*loc)
                 sc = torch.stack([self.scores[(r, s)] for r, s in it.forks]) if len(loc) > 1 else \
                     self.scores[it.forks[0]].view(1, -1)
-                if e2e is not None:
+                if e2e is not None:  # the PRM scores come from the host, the parent maps go back
                     sc = sc.cpu().pin_memory().to(self.dev, non_blocking=True)
+                if forks is not None:
+                    f0 = torch.cuda.Event(enable_timing=True)
+                    f0.record(cur)
                 self._chk(lib.tts_beam_select_fork(h, len(loc), arr, sc.data_ptr(), c.M,
                                                    self.parent.data_ptr(), st), "select_fork")
+                if forks is not None:
+                    f1 = torch.cuda.Event(enable_timing=True)
+                    f1.record(cur)
+                    forks.append((f0, f1))
                 if e2e is not None:
                     e2e["d2h"] += self.parent[: len(loc)].numel() * 4
+                    e2e["h2d"] += sc.numel() * 4
                     e2e["parents"].append(self.parent[: len(loc)].to("cpu", non_blocking=True))
         if e2e is not None:
-            e2e["last_out"].copy_(self.out, non_blocking=True)
-            e2e["d2h"] += self.out.numel() * 4
+            e2e["pipe"].drain()
         for r in self.greqs:
             self._chk(lib.tts_block_table_release_request(h, self.local[r], st), "release")
 
@@ -352,7 +416,7 @@ class SpanBench:
             from paper_2509_00195_b200.tts import TTSError
             raise TTSError(code, what)
 
-    def run_step(self, stats_accum=None, e2e=None, seg=None):
+    def run_step(self, stats_accum=None, e2e=None, seg=None, forks=None):
         from paper_2509_00195_b200.dist import select_fork_global
         c, lib, h, st = self.cfg, self.lib, self.h, self.stream
         k, v = self.prompt
@@ -364,11 +428,12 @@ class SpanBench:
             if seg is not None and open_ev is None:
                 open_ev = torch.cuda.Event(enable_timing=True)
                 open_ev.record(torch.cuda.current_stream(self.dev))
+            out = self.out
             if e2e is not None:
                 hq, hk, hv = e2e["ring"][it.t % nr]
-                q, k, v = e2e["pipe"].stage(hq, hk, hv)
+                q, k, v, out = e2e["pipe"].stage(hq, hk, hv)
             self._chk(lib.tts_decode_step(h, 1, self.req, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
-                                          self.scale, self.out.data_ptr(), st), "decode_step")
+                                          self.scale, out.data_ptr(), st), "decode_step")
             if e2e is not None:
                 e2e["pipe"].release()
             if stats_accum is not None:
@@ -384,74 +449,182 @@ class SpanBench:
                 sc = self.scores[s]
                 if e2e is not None:
                     sc = sc.cpu().pin_memory().to(self.dev, non_blocking=True)
+                    e2e["h2d"] += sc.numel() * 4
                     e2e["d2h"] += c.N * 4
+                if forks is not None:
+                    f0 = torch.cuda.Event(enable_timing=True)
+                    f0.record(torch.cuda.current_stream(self.dev))
                 if self.world > 1:
                     select_fork_global(self.ctx, 0, sc, c.M)
                 else:
                     self.ctx.tts_beam_select_fork([0], sc.view(1, -1), c.M)
+                if forks is not None:
+                    f1 = torch.cuda.Event(enable_timing=True)
+                    f1.record(torch.cuda.current_stream(self.dev))
+                    forks.append((f0, f1))
         if e2e is not None:
-            e2e["last_out"].copy_(self.out, non_blocking=True)
-            e2e["d2h"] += self.out.numel() * 4
+            e2e["pipe"].drain()
         self._chk(lib.tts_block_table_release_request(h, 0, st), "release")
 
 
-def cpu_baseline(cfg, seconds):
-    """The oracle as it stands, on a bounded sample: the first decode iterations
-    of request 0 with full attention (all active beams x all layers) per
-    iteration, until ~`seconds` of CPU work."""
+# ---------------------------------------------------------------------------
+# CPU baseline: the fp64 oracle as it stands (oracle/run.py), on a bounded
+# sample of the same workload (SURVEY 8(d) "Oracle beside it").
+_ORC = {}
+
+
+def _oracle_task(task):
+    """Worker: one oracle attention call, OracleRun.beam_output, for a beam
+    whose token-identity list is given (one layer).  Returns its duration."""
+    cfg, r, b, t, l, ident = task
+    torch.set_num_threads(1)
     from oracle.run import OracleRun
-    torch.set_num_threads(os.cpu_count() or 1)
-    orc = OracleRun(cfg.with_(R=1), num_pages=None, track_content=False)
+    orc = _ORC.get(cfg.name)
+    if orc is None:
+        orc = _ORC[cfg.name] = OracleRun(cfg.with_(R=r + 1), track_content=False)
+        orc.lists = {}
+    orc.lists[r] = {b: ident}
     t0 = time.perf_counter()
-    n_iters = 0
-    steps = 0
-    state = {"stop": False}
+    orc.beam_output(r, b, t, l)
+    return time.perf_counter() - t0
 
-    def sample(it):
-        nonlocal n_iters, steps
-        if state["stop"]:
-            return []
-        n_iters += 1
-        pts = [(r, b, l) for k, r in enumerate(it.reqs) for b in range(cfg.N) if it.active[k][b]
-               for l in range(cfg.L)]
-        steps += len(pts) // cfg.L
-        return pts
 
-    class Stop(Exception):
-        pass
-
-    it_count = 0
+def _cpu_model():
     try:
-        orc.install()
-        for it in workload.schedule(cfg.with_(R=1), [0]):
-            orc.sim.append(it.reqs, [a.tolist() for a in it.active], None)
-            for k, r in enumerate(it.reqs):
-                for b in np.nonzero(it.active[k])[0]:
-                    orc.lists[r][b] = np.concatenate([orc.lists[r][b], [[it.t, b]]])
-            for (r, b, l) in sample(it):
-                orc.beam_output(r, b, it.t, l)
-            it_count += 1
-            if time.perf_counter() - t0 > seconds:
-                break
-    except Stop:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
         pass
-    dt = time.perf_counter() - t0
-    return {"value": steps / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
-            "sample": f"{cfg.name}: first {it_count} decode iterations of one request, fp64 attention for "
-                      f"all {cfg.N} beams x {cfg.L} layers per iteration ({steps} beam-steps, {dt:.1f} s)"}
+    return "?"
+
+
+def cpu_baseline(cfg, seconds, cores=None):
+    """The oracle as it stands, timed on the host cores on a bounded sample:
+    * the block-table simulator + per-beam identity lists over the schedule of
+      request 0 (every append and EVERY fork, each fork timed; stopped and
+      extrapolated per position if it exceeds a third of the budget);
+    * fp64 attention (OracleRun.beam_output) at the first, middle and last
+      position of every TTS step, on a spread subset of the active beams and
+      one layer (all layers cost the same), run once on one core and once on
+      all cores (a process pool, one thread per process); per-position cost is
+      interpolated linearly within each step and multiplied by the active beams
+      and L layers (the extrapolation factor is returned).
+    beam-steps/s = beam-steps / (attention estimate + simulator time)."""
+    import multiprocessing as mproc
+
+    from oracle.run import OracleRun
+    cores = cores or len(os.sched_getaffinity(0))
+    c1 = cfg.with_(R=1)
+    sched = list(workload.schedule(c1, [0]))
+    orc = OracleRun(c1, track_content=False)
+    orc.install()
+    # --- pass 1: simulator (appends, forks) and the sample positions
+    steps_pos = []          # per TTS step: its iterations
+    cur = []
+    for it in sched:
+        cur.append(it.t)
+        if it.forks or it is sched[-1]:
+            steps_pos.append(cur)
+            cur = []
+    want = set()
+    for pos in steps_pos:
+        want.update({pos[0], pos[len(pos) // 2], pos[-1]})
+    tasks, fork_s = [], []
+    t_sim = 0.0
+    done_pos = 0
+    budget_sim = seconds / 3
+    n_beam_sample = 4
+    active_n = {}
+    for it in sched:
+        t0 = time.perf_counter()
+        orc.sim.append(it.reqs, [a.tolist() for a in it.active], None)
+        act = it.active[0]
+        idx = np.nonzero(act)[0]
+        for b in idx:
+            orc.lists[0][b] = np.concatenate([orc.lists[0][b], [[it.t, b]]])
+        t_sim += time.perf_counter() - t0
+        active_n[it.t] = int(act.sum())
+        done_pos += 1
+        if it.t in want and len(idx):
+            pick = idx[np.linspace(0, len(idx) - 1, min(n_beam_sample, len(idx))).astype(int)]
+            for b in sorted(set(pick.tolist())):
+                tasks.append((c1, 0, int(b), it.t, 0, orc.lists[0][b].copy()))
+        if it.forks:
+            t0 = time.perf_counter()
+            sc = workload.scores(c1, 0, it.forks[0][1]).tolist()
+            parents = orc.sim.fork([0], [sc], c1.M)[0]
+            orc.lists[0] = [orc.lists[0][parents[c]].copy() for c in range(c1.N)]
+            dt = time.perf_counter() - t0
+            fork_s.append(dt)
+            t_sim += dt
+        if t_sim > budget_sim and it is not sched[-1]:
+            break
+    n_pos_total = len(sched)
+    beam_steps_total = sum(int(it.active[0].sum()) for it in sched)
+    sim_extrap = n_pos_total / done_pos
+    t_sim_total = t_sim * sim_extrap
+    # --- pass 2: attention samples, one core then all cores
+    tasks = [tk for tk in tasks if tk[3] <= sched[done_pos - 1].t]
+    ctx = mproc.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        pool.map(_oracle_task, tasks[:1] * cores, chunksize=1)   # warm every worker (imports, prompt K/V)
+        per = pool.map(_oracle_task, [tasks[0], tasks[-1]])      # calibrate
+        est = max(1e-4, sum(per) / 2)
+        keep = max(cores, min(len(tasks), int(seconds / 3 / est * cores)))
+        sel = sorted(set(np.linspace(0, len(tasks) - 1, keep).astype(int).tolist()))
+        tasks = [tasks[i] for i in sel]
+        w0 = time.perf_counter()
+        pool.map(_oracle_task, tasks, chunksize=1)
+        wallc = time.perf_counter() - w0
+    # one core: an evenly spaced subset of the same calls (~ a third of the budget)
+    keep1 = max(2, min(len(tasks), int(seconds / 3 / est)))
+    tasks1 = [tasks[i] for i in sorted(set(np.linspace(0, len(tasks) - 1, keep1).astype(int).tolist()))]
+    with ctx.Pool(1) as pool:
+        pool.map(_oracle_task, tasks1[:1])
+        w0 = time.perf_counter()
+        dur1 = pool.map(_oracle_task, tasks1)
+        wall1 = time.perf_counter() - w0
+    speedup = max(1.0, (len(tasks) / wallc) / (len(tasks1) / wall1))
+    # per-position single-core attention cost: mean over the position's sampled
+    # beams x active beams x L, interpolated linearly between sampled positions
+    per_pos = {}
+    for tk, d in zip(tasks1, dur1):
+        per_pos.setdefault(tk[3], []).append(d)
+    xs = sorted(per_pos)
+    ys = [float(np.mean(per_pos[x])) for x in xs]
+    t_attn1 = 0.0
+    for it in sched:
+        t_attn1 += float(np.interp(it.t, xs, ys)) * active_n.get(it.t, int(it.active[0].sum())) * cfg.L
+    value_1 = beam_steps_total / (t_attn1 + t_sim_total)
+    value_c = beam_steps_total / (t_attn1 / speedup + t_sim_total)
+    n_attn_calls = sum(int(it.active[0].sum()) for it in sched) * cfg.L
+    return {"value": value_c, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1core": value_1, "cores_1core": 1, "cpu_model": _cpu_model(),
+            "host_cores": os.cpu_count(), "parallel_speedup": speedup,
+            "fork_us_per_call": 1e6 * float(np.mean(fork_s)) if fork_s else None, "forks_timed": len(fork_s),
+            "sample": (f"{cfg.name}, request 0: block-table simulator + identity lists over "
+                       f"{done_pos}/{n_pos_total} positions (x{sim_extrap:.2f} extrapolated, {len(fork_s)} forks "
+                       f"each timed, {t_sim:.1f} s); fp64 attention at the first/middle/last position of every "
+                       f"TTS step on a spread subset of <= {n_beam_sample} active beams, layer 0: {len(tasks)} "
+                       f"(beam, layer) calls on {cores} cores (process pool, {wallc:.1f} s), {len(tasks1)} of them "
+                       f"on 1 core ({wall1:.1f} s); the run has {n_attn_calls} such calls "
+                       f"(extrapolation x{n_attn_calls / max(1, len(tasks1)):.0f}, linear in position within a step)")}
 
 
 def run_reference(args):
     ws, rank, local = dist_init(args.gpus)
     if rank != 0:
         return
-    cfg = workload.CONFIGS[args.config]
+    cfg = workload.CONFIGS[resolve_config(args, ws)]
     t0 = time.perf_counter()
     vals = []
+    # each step a bounded sample; the whole K + W run stays within a few minutes
+    per = min(args.cpu_seconds, max(3.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_baseline(cfg, min(args.cpu_seconds, 5.0))
+        cpu_baseline(cfg, min(per, 3.0))
     for _ in range(args.steps):
-        vals.append(cpu_baseline(cfg, args.cpu_seconds / max(args.steps, 1)))
+        vals.append(cpu_baseline(cfg, per))
     v = statistics.median([x["value"] for x in vals])
     cb = dict(vals[-1])
     cb["value"] = v
@@ -465,19 +638,41 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def position_bound(per_call, cfg, read_gbs, tc_flops, mufu_per_s):
+    """per decode call (one position of the call's requests, all
+    layers) the time bound max(U / BW, F / TC, E / MUFU) -- U unique KV bytes
+    (+ q, out), F = 4 d Hq L x (sum of active lengths) FLOPs of QK^T and PV, E =
+    Hq L x (sum of active lengths) exponentials.  Returns (sum of bounds in s,
+    the fraction of calls each resource bounds)."""
+    u = per_call[:, 0].astype(np.float64)
+    lg = per_call[:, 1].astype(np.float64)
+    kv_tok = 4 * cfg.Hkv * cfg.d * cfg.L
+    t_mem = u * kv_tok / (read_gbs * 1e9)
+    t_mma = 4.0 * cfg.d * cfg.Hq * cfg.L * lg / tc_flops
+    t_exp = cfg.Hq * cfg.L * lg / mufu_per_s
+    tb = np.maximum(np.maximum(t_mem, t_mma), t_exp)
+    n = max(1, len(tb))
+    which = {"hbm": float((t_mem >= np.maximum(t_mma, t_exp)).sum() / n),
+             "tensor": float((t_mma > np.maximum(t_mem, t_exp)).sum() / n),
+             "mufu": float((t_exp > np.maximum(t_mem, t_mma)).sum() / n)}
+    return float(tb.sum()), which
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     ws, rank, local = dist_init(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = workload.CONFIGS[args.config]
-    rot = args.rotate or DEFAULT_ROTATE[args.config]
+    cname = resolve_config(args, ws)
+    cfg = workload.CONFIGS[cname]
+    rot = args.rotate or DEFAULT_ROTATE[cname]
     if args.tts_steps:
         cfg = cfg.with_(n_steps=args.tts_steps)
     ppr = args.pages_per_request
-    span = args.config == "C5"
+    span = cname == "C5"
     if span:
         # one request, its N beams spread over the ranks; global top-K each step
         scaling = "strong"
@@ -494,7 +689,6 @@ def main():
             cfg = cfg.with_(R=16)
         greqs = [r for r in range(cfg.R) if r % ws == rank]
         scaling = "strong"
-        # page budget: runner.pages_per_request (override with --pages-per-request)
     else:
         cfg = cfg.with_(R=rot * ws)  # independent requests of the same shape, rot per rank
         greqs = [rank * rot + i for i in range(rot)]
@@ -503,6 +697,15 @@ def main():
         b = Bench(cfg, greqs, local, pages_per_request=ppr)
     st = torch.cuda.current_stream(dev)
 
+    # read-only HBM stream peak of this device (the attention
+    # kernel's read roofline, beside the copy peak of MEASURED_PEAKS.json)
+    from paper_2509_00195_b200 import tts as tts_mod
+    probe = torch.empty(4 << 30, dtype=torch.uint8, device=dev)
+    probe.fill_(1)
+    read_gbs = max(tts_mod.stream_read_gbs(probe, 10) for _ in range(3))
+    del probe
+    torch.cuda.empty_cache()
+
     # warm-up (the first one also accumulates the unique / logical KV statistics)
     per_call = torch.zeros(b.n_calls, 2, dtype=torch.int64, device=dev)  # unique / logical tokens per call
     for i in range(max(args.warmup, 1)):
@@ -510,12 +713,13 @@ def main():
     torch.cuda.synchronize(dev)
     st_code = b.ctx.tts_device_status()
     assert st_code == 0, f"device status {st_code} during warm-up"
-    unique_tok, logical_tok = [int(x) for x in per_call.sum(0).tolist()]
+    per_call_np = per_call.cpu().numpy()
+    unique_tok, logical_tok = [int(x) for x in per_call_np.sum(0).tolist()]
     kv_tok = 4 * cfg.Hkv * cfg.d * cfg.L  # bytes per token over all layers (bf16 K+V)
     if args.dump_call_bytes:
         # algorithmic bytes of every attention launch of one step (to line up with ncu launch ids)
         active_rows = [int(a.sum()) for it in b.sched for a in (it.active if not b.batched else [np.stack(it.active)])]
-        calls = per_call[:, 0].tolist()
+        calls = per_call_np[:, 0].tolist()
         json.dump({"config": cfg.name, "kv_bytes_per_token": kv_tok,
                    "qo_bytes_per_beam": cfg.L * cfg.Hq * cfg.d * 6,
                    "unique_kv_bytes": [u * kv_tok for u in calls], "active_beams": active_rows},
@@ -546,22 +750,23 @@ def main():
     # kernel-duration pass: the same K steps again, with a CUDA event pair on the
     # launching stream around every run of decode calls between two forks (the
     # decode-step kernels: k_plan + k_tree_umma per call, k_alloc on page
-    # crossings).  Events between individual calls would serialise the
-    # programmatic-dependent-launch overlap of consecutive calls, so they are
-    # only placed where a fork breaks the chain anyway.
-    segs = []
+    # crossings) and around every select + fork.  Events between individual
+    # calls would serialise the programmatic-dependent-launch overlap of
+    # consecutive calls, so they are only placed where a fork breaks it anyway.
+    segs, fks = [], []
     barrier(ws)
     torch.cuda.synchronize(dev)
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(st)
     for _ in range(args.steps):
-        b.run_step(seg=segs)
+        b.run_step(seg=segs, forks=fks)
     p1.record(st)
     torch.cuda.synchronize(dev)
     barrier(ws)
     ms_prof = p0.elapsed_time(p1)
     attn_ms = sum(a.elapsed_time(z) for a, z in segs)
+    fork_us = [a.elapsed_time(z) * 1e3 for a, z in fks]
     attn_launches = b.n_calls * args.steps
     assert b.ctx.tts_device_status() == 0, "device status error in profiled pass"
 
@@ -569,46 +774,60 @@ def main():
     total_steps = allsum(b.beam_steps * args.steps, ws, dev)
     value = total_steps / (ms_max / 1e3)
     pk, pk_src = peaks()
-    achieved_gbs = (unique_b + qo_b) * args.steps / (attn_ms / 1e3) / 1e9
-    unique_gbs = unique_b * args.steps / (attn_ms / 1e3) / 1e9
-    logical_gbs = logical_b * args.steps / (attn_ms / 1e3) / 1e9
+    attn_s = attn_ms / 1e3
+    achieved_gbs = (unique_b + qo_b) * args.steps / attn_s / 1e9
+    unique_gbs = unique_b * args.steps / attn_s / 1e9
+    logical_gbs = logical_b * args.steps / attn_s / 1e9
+    pj = {}
+    pkf = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pkf):
+        pj = json.load(open(pkf))
+    tc = float(pj.get("bf16_tflops_sustained", 1407.4)) * 1e12
+    sm_mhz = (clk or {}).get("sm_mhz") or float(pj.get("sm_max_mhz", 1965.0))
+    mufu = torch.cuda.get_device_properties(dev).multi_processor_count * 16 * sm_mhz * 1e6
+    tb, tb_which = position_bound(per_call_np, cfg, read_gbs, tc, mufu)
+    tb *= args.steps
 
-    # e2e: same metric through the C-ABI with host buffers (pinned), H2D of every
-    # iteration's q/k/v and the fork scores, D2H of the parent maps and the final output
+    # e2e: the same metric through the C-ABI with host buffers (pinned): every
+    # call's q/k/v H2D and its output D2H (overlapped with the kernels on two
+    # copy streams), the fork scores H2D and the parent maps D2H
     e2e = None
     if args.e2e_steps > 0:
         ring = [(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()) for q, k, v in b.ring]
         q0, k0, v0 = b.ring[0]
-        ctx_e = {"ring": ring, "pipe": H2DPipe((q0, k0, v0), dev),
-                 "d2h": 0, "parents": [], "last_out": torch.empty(b.out.shape, dtype=torch.float32).pin_memory()}
-        h2d = sum(1 for it in b.sched for _ in (it.reqs if not b.batched else [0])) * \
-            (q0.numel() * 2 + k0.numel() * 2 + v0.numel() * 2)
-        h2d += sum(len(it.forks) for it in b.sched) * cfg.N * 4
+        pipe = IOPipe((q0, k0, v0), b.out, dev)
+        ctx_e = {"ring": ring, "pipe": pipe, "d2h": 0, "h2d": 0, "parents": []}
+        n_in = sum(1 for it in b.sched for _ in (it.reqs if not b.batched else [0]))
         barrier(ws)
         torch.cuda.synchronize(dev)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
         for _ in range(args.e2e_steps):
-            ctx_e["d2h"] = 0
             b.run_step(e2e=ctx_e)
         t1.record(st)
         torch.cuda.synchronize(dev)
         ems = allmax(t0.elapsed_time(t1), ws, dev)
+        h2d = n_in * (q0.numel() * 2 + k0.numel() * 2 + v0.numel() * 2) * args.e2e_steps + ctx_e["h2d"]
+        d2h = pipe.d2h_bytes + ctx_e["d2h"]
         e2e = {"value": allsum(b.beam_steps * args.e2e_steps, ws, dev) / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(ctx_e["d2h"])}
+               "h2d_bytes_per_step": int(h2d / args.e2e_steps), "d2h_bytes_per_step": int(d2h / args.e2e_steps),
+               "note": ("through tts_decode_step / tts_beam_select_fork with host buffers: every call's q/k/v "
+                        "copied H2D and its fp32 output D2H (pinned, two copy streams overlapping the kernels), "
+                        "PRM scores H2D and parent maps D2H per fork; bound by PCIe, not by the kernels")}
 
     # DRAM traffic of one ncu --set full capture of this kernel on this workload
     # (profiles/ncu_traffic_<cfg>.json, written by tools/profile_summary.py),
     # scaled to this run's average launch by the captured launch's traffic /
     # algorithmic-bytes ratio (1.0 = every unique page read from HBM exactly once)
-    traffic, traffic_ratio = None, None
-    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    traffic, traffic_algo, traffic_src = None, None, None
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cname}.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            traffic_ratio = pj["dram_bytes_per_launch"] / pj["algo_bytes_of_that_launch"]
-            traffic = traffic_ratio * (unique_b + qo_b) / max(1, b.n_calls)
+            pjf = json.load(open(prof))
+            traffic = float(pjf["dram_bytes_per_launch"])
+            traffic_algo = float(pjf["algo_bytes_of_that_launch"])
+            traffic_src = f"profiles/ncu_traffic_{cname}.json ({pjf.get('tag', '?')}: one --set full capture)"
         except Exception:
             traffic = None
 
@@ -625,25 +844,40 @@ def main():
                        "L": cfg.L, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d, "page": cfg.P,
                        "prompt": cfg.prompt, "steps_x_len": f"{cfg.n_steps}x{cfg.step_len or 'lognormal'}",
                        "beam_steps_per_rank_step": b.beam_steps,
-                       "l2": (f"rotation over {len(greqs)} independent requests, one per call" if not b.batched
-                              else "batched requests (working set >> L2)"),
+                       "l2": (f"unique KV per call {unique_b / max(1, b.n_calls) / 1e6:.0f} MB vs 126 MB L2; "
+                              + (f"rotation over {len(greqs)} independent requests, one per call" if not b.batched
+                                 else "batched requests")),
                        "parallelism": (f"beam-sharded x{ws} (one request's beams span the ranks; NCCL all-gather "
                                        "of scores + lineage migration per step)" if span else
                                        f"dp{ws} (independent requests per rank, no data-path collective)")},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": pk, "unit": "GB/s",
-                         "frac": achieved_gbs / pk, "traffic": traffic, "traffic_over_algo": traffic_ratio,
+                         "frac": achieved_gbs / pk, "traffic": traffic,
+                         "traffic_algo_bytes_of_captured_launch": traffic_algo,
+                         "traffic_over_algo": (traffic / traffic_algo) if traffic and traffic_algo else None,
+                         "traffic_source": traffic_src,
                          "peak_source": pk_src,
                          "kernel": "decode step: k_plan (a2 append + a3 plan) + k_tree_umma (a4/a5 tcgen05 "
                                    "prefix-shared attention), PDL-chained; + k_alloc on page crossings",
                          "algo_bytes": "unique KV (valid tokens of distinct pages) + q bf16 + out fp32",
-                         "unique_kv_gbs": unique_gbs, "logical_kv_gbs": logical_gbs,
-                         "reuse": logical_tok / max(unique_tok, 1),
+                         "algo_bytes_per_launch": (unique_b + qo_b) / max(1, b.n_calls),
+                         "read_peak_gbs_measured": read_gbs,
+                         "frac_of_read_peak": achieved_gbs / read_gbs,
+                         "unique_kv_gbs": unique_gbs, "unique_kv_frac_of_8tbs": unique_gbs / HBM_SPEC_GBS,
+                         "unique_kv_frac_of_read_peak": unique_gbs / read_gbs,
+                         "logical_kv_gbs": logical_gbs, "reuse": logical_tok / max(unique_tok, 1),
+                         "position_bound_ms_per_step": tb * 1e3 / args.steps,
+                         "frac_of_position_bound": tb / attn_s,
+                         "position_bound_by": tb_which,
+                         "position_bound_rates": {"read_gbs": read_gbs, "tensor_tflops": tc / 1e12,
+                                                  "mufu_ex2_per_s": mufu},
                          "attn_ms_per_step": attn_ms / args.steps, "attn_launches_per_step": attn_launches // args.steps,
                          "attn_us_per_launch": attn_ms * 1e3 / max(attn_launches, 1),
                          "attn_share_of_step": attn_ms / ms_prof,
                          "timing": "separate K-step pass, a CUDA event pair on the launching stream around every "
                                    f"run of decode calls between forks ({len(segs)} pairs; "
                                    f"{ms_prof / args.steps:.1f} ms/step with events vs {ms / args.steps:.1f} clean)"},
+            "select_fork_us_per_call": float(np.mean(fork_us)) if fork_us else None,
+            "select_fork_calls_per_step": len(fork_us) // max(1, args.steps),
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -91,7 +91,11 @@ typedef struct {
 /* Caller-owned device buffers (all sizes from tts_query_buffer_bytes). */
 typedef struct {
   void* k_pool;            /* bf16 [L][num_pages][Hkv][P][d]  ("HND" pages) */
-  void* v_pool;            /* bf16 [L][num_pages][Hkv][P][d]                */
+  void* v_pool;            /* fp16 [L][num_pages][Hkv][P][d]: V is stored in
+                              fp16 (reading C14'); the bf16 input
+                              converts exactly for 2^-14 <= |v| < 65520, a
+                              finite |v| >= 65520 raises the sticky
+                              TTS_ERR_UNSUPPORTED (stored as 0)           */
   int32_t* block_tables;   /* [max_requests][max_beams][max_pages_per_beam] */
   int32_t* seq_lens;       /* [max_requests][max_beams] tokens per beam     */
   int32_t* refcounts;      /* [num_pages]                                   */
@@ -162,7 +166,12 @@ tts_status_t tts_prefix_attn_decode(tts_ctx_t ctx, int32_t layer_begin, int32_t 
  * the call is k_alloc (only when a beam crosses a page boundary), k_plan
  * (append + page-list plan) and the persistent attention kernel, chained by
  * programmatic dependent launch; a call's k_plan may run while the previous
- * call's attention kernel still runs (it writes nothing that kernel reads). */
+ * call's attention kernel still runs: its plan goes to the other half of a
+ * double buffer, and the new token lands in a slot the previous call's plan
+ * masks (P = 0 exactly there; the pool never holds a non-finite V).  Every
+ * host-detectable error (unknown or repeated request, page-table capacity,
+ * more than 1024 beam groups) is returned before anything is enqueued or the
+ * host length mirror moves. */
 tts_status_t tts_decode_step(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
                              const uint8_t* active_h, const void* k_new, const void* v_new,
                              const void* q, float softmax_scale, float* out, void* stream);
@@ -221,8 +230,8 @@ tts_status_t tts_beam_select_global(tts_ctx_t ctx, int32_t n_global, const float
 tts_status_t tts_beam_fork_map(tts_ctx_t ctx, int32_t req, int32_t n_new, const int32_t* parent_h,
                                void* stream);
 
-/* Size of a lineage buffer for a beam of `len` tokens:
- * bf16 [2 (K, V)][L][len][Hkv][d]. */
+/* Size of a lineage buffer for a beam of `len` tokens: [2 (K, V)][L][len][Hkv][d]
+ * 16-bit values (K bf16, V fp16 as held in the pools). */
 tts_status_t tts_lineage_bytes(tts_ctx_t ctx, int32_t len, size_t* bytes_h);
 
 /* Copy beam `beam` of request `req` (all its tokens, every layer) into buf
@@ -256,6 +265,13 @@ tts_status_t tts_block_table_stats(tts_ctx_t ctx, int32_t n_req, const int32_t* 
 
 /* Host mirror of a request's beam lengths (no device access). */
 tts_status_t tts_seq_lens_host(tts_ctx_t ctx, int32_t req, int32_t* lens_h);
+
+/* Measurement helper (not part of the method; no context): the HBM read
+ * bandwidth of the current device, from `iters` passes of a read-only 16-B
+ * vector stream over `bytes` of device memory `buf` (make it >> the 126 MB
+ * L2), timed with CUDA events on `stream` (syncs).  The read roofline of the
+ * attention kernel, reported beside the copy peak. */
+tts_status_t tts_stream_read_gbs(const void* buf, size_t bytes, int32_t iters, double* gbs_h, void* stream);
 
 #ifdef __cplusplus
 }

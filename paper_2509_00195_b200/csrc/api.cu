@@ -173,7 +173,17 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
     return TTS_ERR_CUDA;
   }
   for (int i = 0; i < tts::kUploadSlots; ++i) cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  c->tile_cnt_bytes = cnt_bytes;
+  if (const char* s = std::getenv("TTS_ATTN")) c->env_attn_mma = std::strcmp(s, "mma") == 0;
+  if (const char* s = std::getenv("TTS_GROUP_BEAMS")) c->env_group_beams = std::max(0, std::atoi(s));
+  if (const char* s = std::getenv("TTS_NCONS")) c->env_ncons = std::max(0, std::atoi(s));
+  if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::atoi(s) != 0;
+  c->env_no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
   if (!tts::make_tensor_maps(c)) {
+    tts_destroy(c);
+    return TTS_ERR_CUDA;
+  }
+  if (tts::umma_prepare(c) != cudaSuccess) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
   }
@@ -206,6 +216,9 @@ tts_status_t tts_device_status(tts_ctx_t c, void* stream, tts_status_t* out) {
   int32_t v = 0;
   TTS_CUDA(cudaMemcpyAsync(&v, c->buf.status, 4, cudaMemcpyDeviceToHost, st));
   TTS_CUDA(cudaMemsetAsync(c->buf.status, 0, 16, st));
+  // split-tile merge counters back to zero: every kernel after a sticky error
+  // skipped its work, whatever counts a partial launch left behind
+  TTS_CUDA(cudaMemsetAsync(c->ws_tile_cnt, 0, c->tile_cnt_bytes, st));
   TTS_CUDA(cudaStreamSynchronize(st));
   *out = (tts_status_t)v;
   return TTS_OK;
@@ -260,49 +273,65 @@ tts_status_t tts_block_table_init_request(tts_ctx_t c, int32_t req, int32_t n_be
   return TTS_OK;
 }
 
-// Validates, allocates the pages beams crossing a page boundary need (device
-// allocator) and advances the host length mirror.  The K/V write is launched
-// here unless `deferred` is given, in which case the slot list is returned for
-// the fused append + plan kernel of tts_decode_step.
-static tts_status_t append_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
-                                const uint8_t* active, const void* k_new, const void* v_new,
-                                void* stream, std::vector<int32_t>* deferred = nullptr) {
+// a2, host half: validates the call and lists the allocations (beams whose
+// next token opens a page) and the append slots (call index, request, beam,
+// position).  No side effect: nothing is enqueued and the host length mirror
+// is untouched, so a rejected call leaves the context as it was.
+struct AppendPlan {
+  std::vector<tts::AllocItem> items;
+  std::vector<int32_t> slots;  // (i, req, beam, pos) quadruples
+};
+
+static tts_status_t append_plan(tts_ctx_t c, int32_t n_req, const int32_t* req_ids, const uint8_t* active,
+                                const void* k_new, const void* v_new, AppendPlan& ap) {
   if (!c || n_req <= 0 || !req_ids || !k_new || !v_new) return TTS_ERR_INVALID_ARG;
   const tts_config_t& g = c->cfg;
   const int P = g.page_size;
-  std::vector<tts::AllocItem> items;
-  std::vector<int32_t> slots;
+  std::vector<char> seen((size_t)g.max_requests, 0);
   for (int i = 0; i < n_req; ++i) {
     const int r = req_ids[i];
     if (!installed(c, r)) return TTS_ERR_STATE;
+    if (seen[r]) return TTS_ERR_INVALID_ARG;  // a request twice in one call
+    seen[r] = 1;
+  }
+  ap.items.clear();
+  ap.slots.clear();
+  for (int i = 0; i < n_req; ++i) {
+    const int r = req_ids[i];
     for (int b = 0; b < c->n_beams[r]; ++b) {
       if (active && !active[(int64_t)i * g.max_beams + b]) continue;
       const int pos = c->lens[(int64_t)r * g.max_beams + b];
       if (pos / P >= g.max_pages_per_beam) return TTS_ERR_CAPACITY;
-      if (pos % P == 0) items.push_back({entry_of(g, r, b, pos / P), 0, 0});
-      slots.insert(slots.end(), {i, r, b, pos});
+      if (pos % P == 0) ap.items.push_back({entry_of(g, r, b, pos / P), 0, 0});
+      ap.slots.insert(ap.slots.end(), {i, r, b, pos});
     }
   }
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e;
-  if (!items.empty()) {
-    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
-  }
-  if (!slots.empty() && !deferred) {
-    void* d = tts::upload(c, slots.data(), slots.size() * 4, st, &e);
-    TTS_CUDA(e);
-    TTS_CUDA(tts::launch_append_write(c, (const int32_t*)d, (int)slots.size() / 4, n_req,
-                                      (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
-  }
-  for (size_t k = 0; k < slots.size(); k += 4) c->lens[(int64_t)slots[k + 1] * g.max_beams + slots[k + 2]]++;
-  if (deferred) deferred->swap(slots);
   return TTS_OK;
+}
+
+// Advances (+1) or rolls back (-1) the host length mirror over the plan's slots.
+static void mirror_advance(tts_ctx_t c, const AppendPlan& ap, int delta) {
+  for (size_t k = 0; k < ap.slots.size(); k += 4)
+    c->lens[(int64_t)ap.slots[k + 1] * c->cfg.max_beams + ap.slots[k + 2]] += delta;
 }
 
 tts_status_t tts_block_table_append(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
                                     const uint8_t* active, const void* k_new, const void* v_new,
                                     void* stream) {
-  return append_impl(c, n_req, req_ids, active, k_new, v_new, stream);
+  AppendPlan ap;
+  tts_status_t s = append_plan(c, n_req, req_ids, active, k_new, v_new, ap);
+  if (s != TTS_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (!ap.items.empty()) TTS_CUDA(tts::launch_alloc_host(c, ap.items.data(), (int)ap.items.size(), st));
+  if (!ap.slots.empty()) {
+    void* d = tts::upload(c, ap.slots.data(), ap.slots.size() * 4, st, &e);
+    TTS_CUDA(e);
+    TTS_CUDA(tts::launch_append_write(c, (const int32_t*)d, (int)ap.slots.size() / 4, n_req,
+                                      (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
+  }
+  mirror_advance(c, ap, +1);
+  return TTS_OK;
 }
 
 static void prof_pair(tts_ctx_t c, cudaEvent_t* e0, cudaEvent_t* e1);
@@ -344,26 +373,30 @@ static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const ui
   }
 }
 
-// Attention for the call; `pending` (tts_decode_step) carries append slots whose
-// K/V write has not been launched yet: fused with the plan on the tcgen05 path,
-// launched just before the attention kernel otherwise.
-static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_end, int32_t n_req,
-                              const int32_t* req_ids, const uint8_t* active, const void* q, float scale,
-                              float* out, void* stream, const std::vector<int32_t>* pending = nullptr,
-                              const void* k_new = nullptr, const void* v_new = nullptr) {
-  if (!c || !req_ids || !q || !out || n_req <= 0) return TTS_ERR_INVALID_ARG;
+// a3/a4, host half: validates the call and plans the beam groups from the
+// host length mirror.  No side effect.
+struct AttnPlan {
+  bool umma = false;
+  int group_beams = 0;  // mma.sync path: beams per CTA group
+  std::vector<tts::GroupDesc> groups;
+  std::vector<int32_t> glens;  // tcgen05 path: per group beam, current length (0 = inactive)
+};
+
+static tts_status_t attn_prepare(tts_ctx_t c, int32_t layer_begin, int32_t layer_end, int32_t n_req,
+                                 const int32_t* req_ids, const uint8_t* active, AttnPlan& ap) {
+  if (!c || !req_ids || n_req <= 0) return TTS_ERR_INVALID_ARG;
   const tts_config_t& g = c->cfg;
   if (layer_begin < 0 || layer_end > g.num_layers || layer_begin >= layer_end) return TTS_ERR_INVALID_ARG;
-  for (int i = 0; i < n_req; ++i)
+  std::vector<char> seen((size_t)g.max_requests, 0);
+  for (int i = 0; i < n_req; ++i) {
     if (!installed(c, req_ids[i])) return TTS_ERR_STATE;
+    if (seen[req_ids[i]]) return TTS_ERR_INVALID_ARG;
+    seen[req_ids[i]] = 1;
+  }
   const int G = g.num_q_heads / g.num_kv_heads;
   const int n_layers = layer_end - layer_begin;
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e;
-  const char* path = std::getenv("TTS_ATTN");
-  const bool use_umma = tts::umma_supported(c) && !(path && std::strcmp(path, "mma") == 0);
-  std::vector<tts::GroupDesc> groups;
-  if (use_umma) {
+  ap.umma = tts::umma_supported(c) && !c->env_attn_mma;
+  if (ap.umma) {
     // 128-row tiles: balanced runs of <= umma_max_beams beams of one request.
     // The largest groups (a page shared inside a group is staged once) that
     // still give >= 3/4 of a round of tiles for the 2 CTAs per SM of the
@@ -373,7 +406,7 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
     // 59 us (the split pieces cost unequal time: the shared prefix at the head
     // of a tile keeps all four softmax warps busy, a private tail one).
     int maxb = tts::umma_max_beams(c);
-    if (const char* s = std::getenv("TTS_GROUP_BEAMS")) maxb = std::max(1, std::min(maxb, std::atoi(s)));
+    if (c->env_group_beams) maxb = std::max(1, std::min(maxb, c->env_group_beams));
     const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;
     auto group_size = [&](int cap) {
       int gb = 1;
@@ -385,54 +418,68 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
       return gb;
     };
     int gb = group_size(maxb);
-    plan_groups(c, n_req, req_ids, active, gb, groups);
-    if (!std::getenv("TTS_GROUP_BEAMS")) {
-      while (gb > 1 && (int64_t)groups.size() * g.num_kv_heads * n_layers < want) {
+    plan_groups(c, n_req, req_ids, active, gb, ap.groups);
+    if (!c->env_group_beams) {
+      while (gb > 1 && (int64_t)ap.groups.size() * g.num_kv_heads * n_layers < want) {
         gb = group_size((gb + 1) / 2);
-        plan_groups(c, n_req, req_ids, active, gb, groups);
+        plan_groups(c, n_req, req_ids, active, gb, ap.groups);
       }
     }
-    std::vector<int32_t> glens;
-    plan_groups(c, n_req, req_ids, active, gb, groups, &glens);
-    if (groups.empty()) return TTS_OK;
-    if ((int)groups.size() > tts::umma_max_groups()) return TTS_ERR_CAPACITY;
+    plan_groups(c, n_req, req_ids, active, gb, ap.groups, &ap.glens);
+    if ((int)ap.groups.size() > tts::umma_max_groups()) return TTS_ERR_CAPACITY;
+    return TTS_OK;
+  }
+  const int bpt = 16 / G;
+  for (int ncons : {8, 4, 2, 1}) {
+    if (ncons * bpt > 32) continue;
+    if (c->env_ncons && ncons != c->env_ncons) continue;
+    plan_groups(c, n_req, req_ids, active, ncons * bpt, ap.groups);
+    ap.group_beams = ncons * bpt;
+    const int64_t ctas = (int64_t)ap.groups.size() * g.num_kv_heads * n_layers;
+    if (c->env_ncons || ctas >= 2ll * c->num_sms) break;
+  }
+  if (!ap.group_beams) return TTS_ERR_UNSUPPORTED;
+  return TTS_OK;
+}
+
+// Launches the attention of a prepared call; `pending` (tts_decode_step)
+// carries append slots whose K/V write has not been launched yet: fused with
+// the plan on the tcgen05 path, launched just before the attention kernel
+// otherwise.
+static tts_status_t attn_launch(tts_ctx_t c, const AttnPlan& ap, int32_t layer_begin, int32_t layer_end,
+                                int32_t n_req, const void* q, float scale, float* out, void* stream,
+                                const std::vector<int32_t>* pending = nullptr, const void* k_new = nullptr,
+                                const void* v_new = nullptr) {
+  const int n_layers = layer_end - layer_begin;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (ap.umma) {
+    if (ap.groups.empty()) return TTS_OK;
     const bool append = pending && !pending->empty();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) prof_pair(c, &e0, &e1);
     if (e0) TTS_CUDA(cudaEventRecord(e0, st));
-    TTS_CUDA(tts::launch_attention_umma(c, groups.data(), (int)groups.size(), glens.data(), (int)glens.size(),
-                                        layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out,
+    TTS_CUDA(tts::launch_attention_umma(c, ap.groups.data(), (int)ap.groups.size(), ap.glens.data(),
+                                        (int)ap.glens.size(), layer_begin, n_layers, n_req,
+                                        (const __nv_bfloat16*)q, scale, out,
                                         append ? (const __nv_bfloat16*)k_new : nullptr,
                                         append ? (const __nv_bfloat16*)v_new : nullptr, st));
     if (e1) TTS_CUDA(cudaEventRecord(e1, st));
     return TTS_OK;
   }
-  const int bpt = 16 / G;
-  int forced = 0;
-  if (const char* s = std::getenv("TTS_NCONS")) forced = std::atoi(s);
-  int chosen = 0;
-  for (int ncons : {8, 4, 2, 1}) {
-    if (ncons * bpt > 32) continue;
-    if (forced && ncons != forced) continue;
-    plan_groups(c, n_req, req_ids, active, ncons * bpt, groups);
-    chosen = ncons;
-    const int64_t ctas = (int64_t)groups.size() * g.num_kv_heads * n_layers;
-    if (forced || ctas >= 2ll * c->num_sms) break;
-  }
-  if (!chosen) return TTS_ERR_UNSUPPORTED;
   if (pending && !pending->empty()) {
     void* ds = tts::upload(c, pending->data(), pending->size() * 4, st, &e);
     TTS_CUDA(e);
     TTS_CUDA(tts::launch_append_write(c, (const int32_t*)ds, (int)pending->size() / 4, n_req,
                                       (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, st));
   }
-  if (groups.empty()) return TTS_OK;
-  void* d = tts::upload(c, groups.data(), groups.size() * sizeof(tts::GroupDesc), st, &e);
+  if (ap.groups.empty()) return TTS_OK;
+  void* d = tts::upload(c, ap.groups.data(), ap.groups.size() * sizeof(tts::GroupDesc), st, &e);
   TTS_CUDA(e);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) prof_pair(c, &e0, &e1);
   if (e0) TTS_CUDA(cudaEventRecord(e0, st));
-  TTS_CUDA(tts::launch_attention(c, (const tts::GroupDesc*)d, (int)groups.size(), chosen * bpt,
+  TTS_CUDA(tts::launch_attention(c, (const tts::GroupDesc*)d, (int)ap.groups.size(), ap.group_beams,
                                  layer_begin, n_layers, n_req, (const __nv_bfloat16*)q, scale, out, st));
   if (e1) TTS_CUDA(cudaEventRecord(e1, st));
   return TTS_OK;
@@ -441,18 +488,33 @@ static tts_status_t attn_impl(tts_ctx_t c, int32_t layer_begin, int32_t layer_en
 tts_status_t tts_prefix_attn_decode(tts_ctx_t c, int32_t layer_begin, int32_t layer_end,
                                     int32_t n_req, const int32_t* req_ids, const uint8_t* active,
                                     const void* q, float scale, float* out, void* stream) {
-  return attn_impl(c, layer_begin, layer_end, n_req, req_ids, active, q, scale, out, stream);
+  if (!c || !q || !out) return TTS_ERR_INVALID_ARG;
+  AttnPlan ap;
+  tts_status_t s = attn_prepare(c, layer_begin, layer_end, n_req, req_ids, active, ap);
+  if (s != TTS_OK) return s;
+  return attn_launch(c, ap, layer_begin, layer_end, n_req, q, scale, out, stream);
 }
 
 tts_status_t tts_decode_step(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
                              const uint8_t* active, const void* k_new, const void* v_new,
                              const void* q, float scale, float* out, void* stream) {
   if (!c || !q || !out) return TTS_ERR_INVALID_ARG;
-  std::vector<int32_t> pending;
-  tts_status_t s = append_impl(c, n_req, req_ids, active, k_new, v_new, stream, &pending);
+  // every host-detectable error before any side effect: the append plan, then
+  // the attention plan on the post-append lengths (mirror advanced, rolled
+  // back if the attention plan rejects the call)
+  AppendPlan app;
+  tts_status_t s = append_plan(c, n_req, req_ids, active, k_new, v_new, app);
   if (s != TTS_OK) return s;
-  return attn_impl(c, 0, c->cfg.num_layers, n_req, req_ids, active, q, scale, out, stream, &pending, k_new,
-                   v_new);
+  mirror_advance(c, app, +1);
+  AttnPlan ap;
+  s = attn_prepare(c, 0, c->cfg.num_layers, n_req, req_ids, active, ap);
+  if (s != TTS_OK) {
+    mirror_advance(c, app, -1);
+    return s;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!app.items.empty()) TTS_CUDA(tts::launch_alloc_host(c, app.items.data(), (int)app.items.size(), st));
+  return attn_launch(c, ap, 0, c->cfg.num_layers, n_req, q, scale, out, stream, &app.slots, k_new, v_new);
 }
 
 static constexpr int kProfPairs = 4096;
@@ -514,13 +576,13 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   for (int i = 0; i < n_req; ++i)
     for (int j = 0; j < i; ++j)
       if (req_ids[i] == req_ids[j]) return TTS_ERR_INVALID_ARG;
+  for (int i = 0; i < n_req; ++i)
+    if (c->n_rows[req_ids[i]] != N) return TTS_ERR_STATE;  // imported lineages pending: use tts_beam_fork_map
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   void* dreq = tts::upload(c, req_ids, (size_t)n_req * 4, st, &e);
   TTS_CUDA(e);
   TTS_CUDA(tts::launch_select(c, (const int32_t*)dreq, n_req, scores, N, M, parent_out, st));
-  for (int i = 0; i < n_req; ++i)
-    if (c->n_rows[req_ids[i]] != N) return TTS_ERR_STATE;  // imported lineages pending: use tts_beam_fork_map
   TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, n_req, N, N, st));
   // parent map back to the host (for the length mirror and the CoW plan)
   std::vector<int32_t> parent((size_t)n_req * g.max_beams);

@@ -54,7 +54,7 @@ constexpr int kMaxGroups = 1024;             // beam groups per call (smem prefi
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 8;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree
+constexpr int kNumBars = 2 * kNS + 9;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree, qtaken
 constexpr int kOffScr = kOffBar + kNumBars * 8 + 16;
 constexpr int kScrItems = 64;                // producer: one batch of 32 units (2 items each)
 constexpr int kOffPre = kOffScr + kScrItems * 16;
@@ -163,6 +163,10 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
   // at the end), so the attention kernel that waits on this grid also waits on
   // every earlier call.
   if (*(volatile int32_t*)p.status) {
+    // sticky error: an empty plan, so that every CTA of the attention kernel
+    // derives the same (empty) schedule from the counts alone
+    if ((int)blockIdx.x < p.n_groups && threadIdx.x == 0) p.counts[blockIdx.x] = 0;
+    __threadfence();
     if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
   }
@@ -322,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   int* s_pre = reinterpret_cast<int*>(bp + kOffPre);  // [n_groups + 1] exclusive prefix of units per group
   int* s_info = reinterpret_cast<int*>(bp + kOffInfo);  // [0] merger flag
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_ofree = b_qready + 8;
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_ofree = b_qready + 8,
+                 b_qtaken = b_ofree + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
@@ -341,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     bar_init(b_qready, 4);
     bar_init(b_ofree, 4);
+    bar_init(b_qtaken, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
@@ -411,11 +417,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   // append + plan) runs; everything below reads what k_plan writes.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 0) {
-    const bool bail = *(volatile int32_t*)p.status != 0;  // sticky error: no work (outputs untouched)
+    // the schedule depends on the plan's counts only (k_plan writes empty
+    // plans under a sticky error), so every CTA of the launch derives the same
+    // one and the split-tile counters always complete
     int run = 0;
     for (int i0 = 0; i0 < p.n_groups; i0 += 32) {
       const int i = i0 + lane;
-      const int u = (i < p.n_groups && !bail) ? (__ldg(p.counts + i) + 1) / 2 : 0;
+      const int u = i < p.n_groups ? (__ldg(p.counts + i) + 1) / 2 : 0;
       int x = u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -569,6 +577,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
       bar_wait(b_qready, pc & 1);  // this piece's Q in TMEM
+      // an empty piece issues no MMA: release its Q explicitly, so that the
+      // softmax warps load the next Q only after this wait (no parity aliasing)
+      if (j1 == j0 && lane == 0) bar_arrive(b_qtaken);
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNS;
         if (lane == 0) TTS_TR(js, 0);
@@ -634,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       piece(0, gi, slab, j0, j1, pslot);
       load_q(gi, slab);
     }
-    int js = 0;
+    int js = 0, n_empty = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
@@ -763,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       // the next piece's Q (every S MMA of this piece has completed), so that
       // its S = Q K^T overlaps this piece's epilogue
       if (pc + 1 < n_pieces) {
+        if (j1 == j0) bar_wait(b_qtaken, (n_empty++) & 1);  // (a non-empty piece: its S MMAs read Q)
         int gi2, slab2, j02, j12, ps2;
         piece(pc + 1, gi2, slab2, j02, j12, ps2);
         load_q(gi2, slab2);
@@ -936,7 +948,33 @@ int umma_max_groups() { return kMaxGroups; }
 
 bool umma_supported(const Ctx* c) {
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
-  return c->cfg.head_dim == kD && c->cfg.page_size == kP && G >= 4 && G <= 16 && c->tmap3_ok && c->tmap_ok;
+  return c->cfg.head_dim == kD && c->cfg.page_size == kP && G >= 4 && G <= 16 && c->tmap3_ok && c->tmap_ok &&
+         c->umma_ok;
+}
+
+// Per device context: the kernel attributes, and the residency the schedule
+// and the plan's double buffer rely on.  The grid is exactly two CTAs per SM
+// and at most two fit per SM, so all CTAs of call N+1 running implies call N's
+// attention kernel has exited -- and call N+2's k_plan (PDL-released by call
+// N+1's CTAs) can only then overwrite the plan buffer call N read.  If a
+// device or build breaks either condition, the context uses the mma.sync path.
+cudaError_t umma_prepare(Ctx* c) {
+  c->umma_ok = false;
+  const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
+  if (c->cfg.head_dim != kD || c->cfg.page_size != kP || G < 4 || G > 16) return cudaSuccess;
+  for (auto k : {k_tree_umma<true>, k_tree_umma<false>}) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    if (occ != 2 || 2 * c->num_sms > kMaxCtas) return cudaSuccess;
+  }
+  c->umma_ok = true;
+  return cudaSuccess;
 }
 
 int umma_max_beams(const Ctx* c) {
@@ -1005,20 +1043,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     pp.glens = (const int32_t*)dl;
   }
   // measured 2% slower on C2/C3 (the softmax is latency-, not MUFU-bound): off unless TTS_POLY=1
-  static const bool poly = std::getenv("TTS_POLY") && std::atoi(std::getenv("TTS_POLY")) != 0;
-  auto kern = poly ? k_tree_umma<true> : k_tree_umma<false>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    for (auto k : {k_tree_umma<true>, k_tree_umma<false>}) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      if (e != cudaSuccess) return e;
-      // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
-      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (e != cudaSuccess) return e;
-    }
-    attr_done = true;
-  }
-  static const bool no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
+  auto kern = c->env_poly ? k_tree_umma<true> : k_tree_umma<false>;
+  const bool no_pdl = c->env_no_pdl;
   cudaLaunchAttribute pdl;
   // each kernel may start while its predecessor on the stream runs; both wait
   // (griddepcontrol.wait) before touching what the predecessor writes
@@ -1037,7 +1063,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   }
   cudaLaunchConfig_t cfg = {};
   // persistent: two CTAs per SM (the smem / TMEM / register budget of one CTA)
-  cfg.gridDim = dim3(std::min(2 * c->num_sms, kMaxCtas));
+  cfg.gridDim = dim3(2 * c->num_sms);  // == 2 x SMs, <= kMaxCtas (umma_prepare)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;

@@ -88,6 +88,14 @@ struct Ctx {
   int plan_parity = 0;
   float* ws_partial = nullptr;     // split tiles' partial (m, l, O) (attention_umma.cu)
   int32_t* ws_tile_cnt = nullptr;  // [num_layers * num_kv_heads * max groups], zero between launches
+  size_t tile_cnt_bytes = 0;
+  // environment toggles (tools / tests), read once in tts_create
+  bool env_attn_mma = false;  // TTS_ATTN=mma: force the mma.sync path
+  int env_group_beams = 0;    // TTS_GROUP_BEAMS: beams per group on the tcgen05 path
+  int env_ncons = 0;          // TTS_NCONS: consumer warps of the mma.sync path
+  bool env_poly = false;      // TTS_POLY=1: polynomial exp2 for every other pair
+  bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
+  bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
 };
 
 // ---- pool value format --------------------------------------------------------
@@ -153,6 +161,9 @@ cudaError_t launch_attention(Ctx* c, const GroupDesc* groups_d, int n_groups, in
 bool make_tensor_maps(Ctx* c);
 // attention_umma.cu (tcgen05 path: d = 128, 4 <= G <= 16)
 bool umma_supported(const Ctx* c);
+// per-device kernel attributes (dynamic smem, carveout) and the occupancy the
+// persistent schedule relies on (2 CTAs per SM); called by tts_create
+cudaError_t umma_prepare(Ctx* c);
 int umma_max_beams(const Ctx* c);
 // One launch per call: a2 (append of the call's new token, when k_new != null)
 // + a3 (plan, built on the fly per CTA) + a4.  groups_h / lens_h are HOST

@@ -52,11 +52,14 @@ def tts_config(cfg: workload.Config, n_req: int, num_pages: Optional[int] = None
 
 
 class Inputs:
-    """Identity-keyed synthetic q / k / v / scores on the device."""
+    """Identity-keyed synthetic q / k / v / scores on the device.  gen_device:
+    where the hash runs ("cpu": generated on the host, bit-identical, then
+    copied -- keeps the device's launch stream to libtts's own kernels)."""
 
-    def __init__(self, cfg: workload.Config, device):
+    def __init__(self, cfg: workload.Config, device, gen_device=None):
         self.cfg = cfg
-        self.dev = device
+        self.out_dev = device
+        self.dev = device if gen_device is None else torch.device(gen_device)
 
     def _idx(self, n, shape_pos, ndim):
         s = [1] * ndim
@@ -70,7 +73,7 @@ class Inputs:
         h = self._idx(c.Hkv, 2, 3)
         k = rng.kv_prompt_values(c.seed, "k", l, req, pos, h, c.d, device=self.dev)
         v = rng.kv_prompt_values(c.seed, "v", l, req, pos, h, c.d, device=self.dev)
-        return k.contiguous(), v.contiguous()
+        return k.contiguous().to(self.out_dev), v.contiguous().to(self.out_dev)
 
     def step(self, t: int, greqs: Sequence[int]):
         """q [L][n][N][Hq][d], k/v [L][n][N][Hkv][d] for global requests greqs."""
@@ -83,15 +86,16 @@ class Inputs:
         q = rng.q_values(c.seed, l, r, t, b, hq, c.d, c.q_scale, device=self.dev)
         k = rng.kv_decode_values(c.seed, "k", l, r, t, b, hk, c.d, device=self.dev)
         v = rng.kv_decode_values(c.seed, "v", l, r, t, b, hk, c.d, device=self.dev)
-        return q.contiguous(), k.contiguous(), v.contiguous()
+        return (q.contiguous().to(self.out_dev), k.contiguous().to(self.out_dev),
+                v.contiguous().to(self.out_dev))
 
     def scores(self, greq: int, step: int):
-        return workload.scores(self.cfg, greq, step, device=self.dev)
+        return workload.scores(self.cfg, greq, step, device=self.dev).to(self.out_dev)
 
 
 class BeamStepRunner:
     def __init__(self, cfg: workload.Config, req_ids: Optional[Sequence[int]] = None, device: int = 0,
-                 num_pages: Optional[int] = None, fused: bool = True):
+                 num_pages: Optional[int] = None, fused: bool = True, gen_device=None):
         self.cfg = cfg
         self.fused = fused
         self.req_ids = list(range(cfg.R)) if req_ids is None else list(req_ids)
@@ -99,7 +103,7 @@ class BeamStepRunner:
         self.tcfg = tts_config(cfg, len(self.req_ids), num_pages)
         self.ctx = Context(self.tcfg, device)
         self.dev = self.ctx.device
-        self.inputs = Inputs(cfg, self.dev)
+        self.inputs = Inputs(cfg, self.dev, gen_device)
         self.scale = 1.0 / math.sqrt(cfg.d)
 
     def install(self):

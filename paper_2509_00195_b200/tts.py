@@ -90,6 +90,8 @@ def load() -> ctypes.CDLL:
         lib.tts_status_str.restype = ctypes.c_char_p
         lib.tts_launch_count.argtypes = [_P]
         lib.tts_launch_count.restype = ctypes.c_int64
+        lib.tts_stream_read_gbs.argtypes = [_P, ctypes.c_size_t, _I, ctypes.POINTER(ctypes.c_double), _P]
+        lib.tts_stream_read_gbs.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -99,6 +101,15 @@ def header_functions() -> list:
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(tts_[a-z0-9_]+)\s*\(", src)))
+
+
+def stream_read_gbs(buf: torch.Tensor, iters: int = 10) -> float:
+    """tts_stream_read_gbs: HBM read bandwidth over the device tensor buf (syncs)."""
+    g = ctypes.c_double()
+    st = ctypes.c_void_p(torch.cuda.current_stream(buf.device).cuda_stream)
+    _check(load().tts_stream_read_gbs(ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(),
+                                      int(iters), ctypes.byref(g), st), "tts_stream_read_gbs")
+    return g.value
 
 
 def status_str(code: int) -> str:
@@ -172,7 +183,7 @@ class Context:
                                dtype=dtype, device=dev)
 
         self.k_pool = buf(sz["k_pool"], torch.bfloat16)
-        self.v_pool = buf(sz["v_pool"], torch.bfloat16)
+        self.v_pool = buf(sz["v_pool"], torch.float16)  # V is held in fp16 (include/tts.h)
         self.block_tables = buf(sz["block_tables"], torch.int32)
         self.seq_lens = buf(sz["seq_lens"], torch.int32)
         self.refcounts = buf(sz["refcounts"], torch.int32)
