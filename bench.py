@@ -367,27 +367,30 @@ class Bench:
 
 class SpanBench:
     """C5: one request whose N beams span the G ranks (n = N / G per rank).
-    Per decode iteration each rank runs append + attention on its n beams;
-    at every step end the ranks all-gather scores and lengths (NCCL), run the
-    same global selection and migrate lineages whose children changed rank
-    (paper_2509_00195_b200.dist.select_fork_global)."""
+    Per decode iteration each rank runs append + attention on its n beams; at
+    every step end libtts runs the cross-rank step on every rank
+    (tts_beam_select_fork_global over its NCCL communicator: all-gather of
+    (score, gid, len), global selection, placement, lineage migration, fork)."""
 
     def __init__(self, cfg, world, rank, dev_index, ring=8):
         from paper_2509_00195_b200 import build
         build.build()
-        from paper_2509_00195_b200.runner import tts_config, Inputs
+        from paper_2509_00195_b200.runner import tts_config, Inputs, pages_per_request
         from paper_2509_00195_b200.tts import Context
         self.cfg, self.world, self.rank = cfg, world, rank
         self.nl = cfg.N // world
         maxb = 2 * self.nl if world > 1 else cfg.N
-        from paper_2509_00195_b200.runner import pages_per_request
         if world == 1:
             pages = pages_per_request(cfg) + 256  # the whole tree on one rank
         else:
-            pages = self.nl * workload.max_pages_per_beam(cfg) + 256  # imported lineages are private copies
+            pages = 2 * self.nl * workload.max_pages_per_beam(cfg) + 256  # imported lineages are private copies
         self.tcfg = tts_config(cfg, 1, num_pages=pages, max_beams=maxb)
         self.ctx = Context(self.tcfg, dev_index)
         self.lib, self.h, self.dev = self.ctx.lib, self.ctx.h, self.ctx.device
+        self.stage = None
+        if world > 1:
+            from paper_2509_00195_b200.dist import nccl_comm
+            self.stage = nccl_comm(self.ctx, stage_bytes=4 << 30)
         self.inp = Inputs(cfg, self.dev)
         self.scale = ctypes.c_float(1.0 / math.sqrt(cfg.d))
         self.batched = False
@@ -401,10 +404,8 @@ class SpanBench:
         self.out = torch.empty(cfg.L, 1, maxb, cfg.Hq, cfg.d, dtype=torch.float32, device=self.dev)
         self.prompt = self.inp.prompt_kv(0)
         self.sched = list(workload.schedule(cfg, [0]))
-        sl = slice(rank * self.nl, (rank + 1) * self.nl)
-        self.scores = {s: self.inp.scores(0, s)[sl].contiguous() for it in self.sched for (_, s) in it.forks}
-        self.act = {}
-        self.beam_steps = sum(int(it.active[0][sl].sum()) for it in self.sched)
+        self.scores = {s: self.inp.scores(0, s).contiguous() for it in self.sched for (_, s) in it.forks}
+        self.beam_steps = sum(int(it.active[0][rank * self.nl:(rank + 1) * self.nl].sum()) for it in self.sched)
         self.n_calls = len(self.sched)
         self.ncall = 0
         self.stream = self.ctx.stream
@@ -417,10 +418,12 @@ class SpanBench:
             raise TTSError(code, what)
 
     def run_step(self, stats_accum=None, e2e=None, seg=None, forks=None):
-        from paper_2509_00195_b200.dist import select_fork_global
         c, lib, h, st = self.cfg, self.lib, self.h, self.stream
         k, v = self.prompt
         self._chk(lib.tts_block_table_init_request(h, 0, self.nl, c.prompt, k.data_ptr(), v.data_ptr(), st), "init")
+        if self.world > 1:
+            from paper_2509_00195_b200.dist import equal_caps
+            self.ctx.tts_span_init(0, c.N, equal_caps(c.N, self.world))
         nr = len(self.ring)
         open_ev = None
         for it in self.sched:
@@ -447,6 +450,8 @@ class SpanBench:
                 open_ev = None
             for (_, s) in it.forks:
                 sc = self.scores[s]
+                if self.world > 1:  # this rank's beams' scores, in its row order (ascending gid)
+                    sc = sc[torch.tensor(self.ctx.tts_span_gids(0), device=self.dev)].contiguous()
                 if e2e is not None:
                     sc = sc.cpu().pin_memory().to(self.dev, non_blocking=True)
                     e2e["h2d"] += sc.numel() * 4
@@ -455,7 +460,7 @@ class SpanBench:
                     f0 = torch.cuda.Event(enable_timing=True)
                     f0.record(torch.cuda.current_stream(self.dev))
                 if self.world > 1:
-                    select_fork_global(self.ctx, 0, sc, c.M)
+                    self.ctx.tts_beam_select_fork_global(0, sc, c.M)
                 else:
                     self.ctx.tts_beam_select_fork([0], sc.view(1, -1), c.M)
                 if forks is not None:
@@ -881,6 +886,7 @@ def main():
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "attention_kernel": b.ctx.attention_kernel(),
             "host_enqueue_ms_per_step": host_s * 1e3 / args.steps,
             "clocks": clk,
         }

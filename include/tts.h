@@ -126,6 +126,12 @@ tts_status_t tts_device_status(tts_ctx_t ctx, void* stream, tts_status_t* out_h)
 /* Number of kernels this context has launched so far (host counter). */
 int64_t tts_launch_count(tts_ctx_t ctx);
 
+/* Name of the attention kernel this context's decode calls launch:
+ * "k_tree_umma" (tcgen05, d = 128, 4 <= G <= 16, two CTAs resident per SM) or
+ * "k_tree_attn" (mma.sync: d = 64, G < 4, or a device where the tcgen05
+ * kernel's residency does not hold). */
+const char* tts_attention_kernel(tts_ctx_t ctx);
+
 /* a1. Install request `req` with n_beams beams on a prompt of prompt_len
  * tokens.  k_prompt / v_prompt: bf16 [L][prompt_len][Hkv][d].
  * Allocates ceil(prompt_len/P) pages (lowest free ids, position order),
@@ -244,6 +250,83 @@ tts_status_t tts_lineage_export(tts_ctx_t ctx, int32_t req, int32_t beam, void* 
  * use; pool exhaustion is the sticky device error. */
 tts_status_t tts_lineage_import(tts_ctx_t ctx, int32_t req, int32_t beam, int32_t len, const void* buf,
                                 void* stream);
+
+/* ---- a8 through the library: libtts-owned communicator --------------------
+ * tts_beam_select_fork_global runs the whole cross-rank step:
+ *   1. all-gather of (score, gid, len) of every local beam (12 B per beam);
+ *   2. the selection kernel over the N gathered scores, the global id as index
+ *      (ledger C19) -> the same parent map on every rank;
+ *   3. placement, identical on every rank: children in gid order stay on
+ *      their parent's rank while its capacity lasts; the overflow, in gid
+ *      order, goes to the lowest rank with free capacity;
+ *   4. migration: each rank imports the whole lineage (K bf16 / V fp16, every
+ *      layer) of every remote parent one of its children needs, in ascending
+ *      parent gid, into spare rows (fresh pages), in rounds that fit the
+ *      staging buffer;
+ *   5. local fork by the explicit parent map (tts_beam_fork_map): new row i =
+ *      the rank's i-th child in ascending gid.
+ * Transports: NCCL (tts_comm_init; libnccl.so.2 is resolved at run time --
+ * the copy PyTorch loaded) or host callbacks (tts_comm_init_host: any byte
+ * transport, e.g. a gloo process group, or threads of one process acting as
+ * ranks).  Every rank of the communicator must make the same sequence of
+ * span calls.  Survivors, parent maps, child -> rank and every beam's token
+ * sequence are identical across runs and equal the single-GPU run; page ids
+ * are per rank (ledger C20). */
+
+/* Host transport: all calls are blocking and collective over the ranks. */
+typedef struct {
+  void* user;
+  /* every rank contributes `bytes` from send_h; recv_h receives nranks * bytes
+   * (rank order).  Returns 0 on success. */
+  int (*allgather)(void* user, const void* send_h, void* recv_h, size_t bytes);
+  /* grouped point-to-point: n_send messages to dst[i] from send_h[i]
+   * (send_bytes[i]) and n_recv messages from src[i] into recv_h[i]
+   * (recv_bytes[i]), matched in order per peer.  Returns 0 on success. */
+  int (*sendrecv)(void* user, int32_t n_send, const int32_t* dst, const void* const* send_h,
+                  const size_t* send_bytes, int32_t n_recv, const int32_t* src, void* const* recv_h,
+                  const size_t* recv_bytes);
+} tts_host_transport_t;
+
+/* A fresh NCCL unique id (128 B, host) for rank 0 to broadcast.  TTS_ERR_NCCL
+ * if libnccl.so.2 cannot be loaded. */
+tts_status_t tts_comm_unique_id(void* id_h);
+
+/* Joins the NCCL communicator (nranks, rank) of `id_h` on the context's
+ * device.  stage: caller-owned device buffer (>= 4 KiB; holds the all-gather
+ * records, then the two halves of every migration round). */
+tts_status_t tts_comm_init(tts_ctx_t ctx, const void* nccl_unique_id_128B_h, int32_t nranks, int32_t rank,
+                           void* stage, size_t stage_bytes);
+
+/* Same over a host transport (copied; its user pointer must outlive the
+ * context); libtts allocates a pinned host staging buffer of stage_bytes. */
+tts_status_t tts_comm_init_host(tts_ctx_t ctx, int32_t nranks, int32_t rank, const tts_host_transport_t* t,
+                                size_t stage_bytes);
+
+/* Destroys the context's communicator (also done by tts_destroy). */
+tts_status_t tts_comm_destroy(tts_ctx_t ctx);
+
+/* Declares installed request `req` as spanning the communicator's ranks:
+ * N = n_global beams, rank r holds caps_h[r] of them (sum = N, N <= 1024,
+ * 2 * caps[r] <= max_beams for spare rows); this rank's rows are the
+ * contiguous global ids [sum(caps[:rank]), sum(caps[:rank+1])) -- at install
+ * every beam holds only the prompt, so the cut is byte-balanced.  The request
+ * must have been installed with caps_h[rank] beams. */
+tts_status_t tts_span_init(tts_ctx_t ctx, int32_t req, int32_t n_global, const int32_t* caps_h);
+
+/* Global ids of this rank's rows of a spanning request (host int32 [n_local]). */
+tts_status_t tts_span_gids(tts_ctx_t ctx, int32_t req, int32_t* gids_h);
+
+/* The cross-rank select + fork of a spanning request (steps 1-5 above;
+ * collective: every rank calls it).  local_scores: device fp32 [n_local]
+ * (row order).  parent_gid_out (device int32 [N], nullable): new gid -> old
+ * gid.  child_rank_out (device int32 [N], nullable).  Syncs. */
+tts_status_t tts_beam_select_fork_global(tts_ctx_t ctx, int32_t req, const float* local_scores, int32_t width_m,
+                                         int32_t* parent_gid_out, int32_t* child_rank_out, void* stream);
+
+/* Placement rule alone (host only, no context): child gid -> rank from the
+ * parent map (parent_gid_h [N]), the old gid -> rank map and the capacities. */
+tts_status_t tts_span_placement(int32_t n_global, const int32_t* parent_gid_h, const int32_t* old_rank_h,
+                                int32_t nranks, const int32_t* caps_h, int32_t* child_rank_h);
 
 /* Release every page of request `req` (refcount decrement, free at 0). */
 tts_status_t tts_block_table_release_request(tts_ctx_t ctx, int32_t req, void* stream);

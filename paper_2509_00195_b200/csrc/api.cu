@@ -29,6 +29,8 @@ size_t workspace_bytes(const tts_config_t& c) {
   s += align_up(2 * rows * 4);                          // plan counts
   s += align_up(umma_partial_bytes());                  // split tiles' partial states
   s += align_up((size_t)c.num_layers * c.num_kv_heads * umma_max_groups() * 4);  // split-tile counters
+  s += align_up(1024 * 4);                          // global selection: gid-indexed scores
+  s += align_up(1024 * 4);                          // global parent map
   s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
   return s;
 }
@@ -167,6 +169,10 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   c->ws_tile_cnt = (int32_t*)w;
   const size_t cnt_bytes = (size_t)cfg->num_layers * cfg->num_kv_heads * tts::umma_max_groups() * 4;
   w += tts::align_up(cnt_bytes);
+  c->ws_scores_all = (float*)w;
+  w += tts::align_up(1024 * 4);
+  c->ws_parent_all = (int32_t*)w;
+  w += tts::align_up(1024 * 4);
   c->ws_upload = w;
   if (cudaMallocHost(&c->pinned, (size_t)tts::kUploadSlots * tts::kUploadSlotBytes) != cudaSuccess) {
     delete c;
@@ -177,8 +183,9 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_ATTN")) c->env_attn_mma = std::strcmp(s, "mma") == 0;
   if (const char* s = std::getenv("TTS_GROUP_BEAMS")) c->env_group_beams = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("TTS_NCONS")) c->env_ncons = std::max(0, std::atoi(s));
-  if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::atoi(s) != 0;
+  if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::max(0, std::min(2, std::atoi(s)));
   c->env_no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
+  if (const char* s = std::getenv("TTS_CTAS_PER_SM")) c->env_ctas_per_sm = std::atoi(s) == 1 ? 1 : 2;
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
@@ -199,6 +206,7 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
 tts_status_t tts_destroy(tts_ctx_t c) {
   if (!c) return TTS_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
+  tts_comm_destroy(c);
   for (int i = 0; i < tts::kUploadSlots; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   for (auto& e : c->prof_ev)
@@ -209,6 +217,12 @@ tts_status_t tts_destroy(tts_ctx_t c) {
 }
 
 int64_t tts_launch_count(tts_ctx_t c) { return c ? c->launches : -1; }
+
+const char* tts_attention_kernel(tts_ctx_t c) {
+  if (!c) return "";
+  if (tts::umma_supported(c) && !c->env_attn_mma) return "k_tree_umma";
+  return "k_tree_attn";
+}
 
 tts_status_t tts_device_status(tts_ctx_t c, void* stream, tts_status_t* out) {
   if (!c || !out) return TTS_ERR_INVALID_ARG;
@@ -703,6 +717,7 @@ tts_status_t tts_block_table_release_request(tts_ctx_t c, int32_t req, void* str
   if (!c) return TTS_ERR_INVALID_ARG;
   if (!installed(c, req)) return TTS_ERR_STATE;
   TTS_CUDA(tts::launch_release(c, req, c->n_rows[req], (cudaStream_t)stream));
+  c->spans.erase(req);
   c->n_beams[req] = 0;
   c->n_rows[req] = 0;
   std::fill(c->lens.begin() + (int64_t)req * c->cfg.max_beams,

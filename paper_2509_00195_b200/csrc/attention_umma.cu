@@ -55,12 +55,37 @@ constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
 constexpr int kNumBars = 2 * kNS + 9;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree, qtaken
-constexpr int kOffScr = kOffBar + kNumBars * 8 + 16;
+constexpr int kOffScr = (kOffBar + kNumBars * 8 + 16 + 15) / 16 * 16;  // int4 scratch: 16-B aligned
 constexpr int kScrItems = 64;                // producer: one batch of 32 units (2 items each)
 constexpr int kOffPre = kOffScr + kScrItems * 16;
 constexpr int kOffInfo = kOffPre + (kMaxGroups + 1) * 4;
 constexpr int kSmemBytes = kOffInfo + 16 + 1024;
 static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert(3 * (kSmemBytes + 1024) > 228 * 1024, "at most two CTAs per SM (plan double-buffer argument)");
+static_assert(kOffScr % 16 == 0 && kOffMeta % 16 == 0 && kOffBar % 8 == 0, "shared-memory alignment");
+
+#ifdef TTS_PROF
+// per CTA (last launch) x warp: accumulated cycles [0..5] + counters (tools/prof.py)
+__device__ long long g_prof[512][8][16];
+#define PROF_DECL long long pf_[16] = {}; long long pf_t = clock64()
+#define PROF_MARK(k)                   \
+  do {                                 \
+    const long long t_ = clock64();    \
+    pf_[(k)] += t_ - pf_t;             \
+    pf_t = t_;                         \
+  } while (0)
+#define PROF_CNT(k) (pf_[(k)] += 1)
+#define PROF_FLUSH(w)                                                   \
+  do {                                                                  \
+    if (blockIdx.x < 512 && (threadIdx.x & 31) == 0)                    \
+      for (int k_ = 0; k_ < 16; ++k_) g_prof[blockIdx.x][(w)][k_] = pf_[k_]; \
+  } while (0)
+#else
+#define PROF_DECL
+#define PROF_MARK(k) do {} while (0)
+#define PROF_CNT(k) do {} while (0)
+#define PROF_FLUSH(w) do {} while (0)
+#endif
 
 #ifdef TTS_TRACE
 __device__ long long g_trace[1024][8];
@@ -78,12 +103,12 @@ __device__ __forceinline__ long long gtimer() {
   } while (0)
 #define TTS_TR(j, ev)                                                                   \
   do {                                                                                  \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
+    if (blockIdx.x == 10 && (j) >= 0 && (j) < 1024) \
       g_trace[(j)][(ev)] = clock64();                                                   \
   } while (0)
 #define TTS_TR2(j, ev)                                                                  \
   do {                                                                                  \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 10 && (j) >= 0 && (j) < 1024) \
+    if (blockIdx.x == 10 && (j) >= 0 && (j) < 1024) \
       g_trace2[(j)][(ev)] = clock64();                                                  \
   } while (0)
 #else
@@ -309,9 +334,9 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 // pieces' partial (m, l, O) in piece order, so the result does not depend on
 // which CTA finishes first.  Every warp derives the same piece sequence from
 // the per-group unit counts (prefix in smem).
-// kPoly: every other pair of exponentials on the FMA/ALU pipes (ex2_poly2)
+// kPoly: exponentials on the FMA/ALU pipes (ex2_poly2) instead of MUFU: 1 = every other pair, 2 = all
 // instead of MUFU.
-template <bool kPoly>
+template <int kPoly>
 __global__ void __launch_bounds__(kThreads, 2)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
@@ -322,7 +347,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   int4* meta = reinterpret_cast<int4*>(bp + kOffMeta);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bp + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  int4* scr = reinterpret_cast<int4*>(bp + kOffScr);
   int* s_pre = reinterpret_cast<int*>(bp + kOffPre);  // [n_groups + 1] exclusive prefix of units per group
   int* s_info = reinterpret_cast<int*>(bp + kOffInfo);  // [0] merger flag
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
@@ -508,6 +532,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 4) {
     // ========================= producer: TMA =========================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+    }
+    // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
+    PROF_DECL;
     int slot = 0;
     uint32_t ph = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
@@ -518,32 +548,40 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int nit = __ldg(p.counts + gi);
       const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
       const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
-      auto issue = [&](const int4& m0, const int4& m1) {  // lane 0
+      // the whole warp runs the issue loop on warp-uniform values (the
+      // unit's pages are broadcast from the lane that loaded them); one
+      // elected lane writes the slot's metadata and issues the TMAs
+      auto issue = [&](const int4& m0, const int4& m1) {
+        PROF_MARK(1);
         bar_wait(b_empty + 8 * slot, ph ^ 1u);
-        meta[slot * kU] = m0;
-        meta[slot * kU + 1] = m1;
-        const uint32_t fb = b_full + 8 * slot;
-        bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
-        const uint32_t sb = base + kOffRing + slot * kSlot;
-        // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
-        // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
-        const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
-        tma2d(sb, &tmk, 0, y0, fb);
-        tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
-        tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
-        if (m1.x >= 0) {
-          const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
-          tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
-          tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
-          tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+        PROF_MARK(0);
+        if (elect_one()) {
+          meta[slot * kU] = m0;
+          meta[slot * kU + 1] = m1;
+          const uint32_t fb = b_full + 8 * slot;
+          bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
+          const uint32_t sb = base + kOffRing + slot * kSlot;
+          // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
+          // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
+          const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
+          tma2d(sb, &tmk, 0, y0, fb);
+          tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
+          tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
+          if (m1.x >= 0) {
+            const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
+            tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
+            tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
+            tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+          }
         }
+        __syncwarp();
         if (++slot == kNS) {
           slot = 0;
           ph ^= 1u;
         }
       };
       // 32 units per batch (lane = unit); the next batch's loads are in
-      // flight while lane 0 issues the current one
+      // flight while the current one is issued
       int4 a0 = make_int4(-2, 0, 0, 0), a1 = a0;
       auto load = [&](int v0) {
         const int v = v0 + lane;
@@ -554,17 +592,21 @@ __global__ void __launch_bounds__(kThreads, 2)
       };
       load(j0);
       for (int v0 = j0; v0 < j1; v0 += 32) {
-        scr[2 * lane] = a0;
-        scr[2 * lane + 1] = a1;
-        __syncwarp();
+        const int4 b0 = a0, b1 = a1;
         if (v0 + 32 < j1) load(v0 + 32);
-        if (lane == 0) {
-          const int n = min(32, j1 - v0);
-          for (int k = 0; k < n; ++k) issue(scr[2 * k], scr[2 * k + 1]);
+        PROF_MARK(2);
+        const int n = min(32, j1 - v0);
+        for (int k = 0; k < n; ++k) {
+          const int4 m0 = make_int4(__shfl_sync(~0u, b0.x, k), __shfl_sync(~0u, b0.y, k), __shfl_sync(~0u, b0.z, k),
+                                    __shfl_sync(~0u, b0.w, k));
+          const int4 m1 = make_int4(__shfl_sync(~0u, b1.x, k), __shfl_sync(~0u, b1.y, k), __shfl_sync(~0u, b1.z, k),
+                                    __shfl_sync(~0u, b1.w, k));
+          issue(m0, m1);
         }
-        __syncwarp();
+        PROF_MARK(1);
       }
     }
+    PROF_FLUSH(4);
   } else if (warp == 5) {
     // ========================= S issuer: S = Q K^T =========================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
@@ -572,21 +614,28 @@ __global__ void __launch_bounds__(kThreads, 2)
     // waits behind the other's issue (the tensor pipe runs both in issue order).
     constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
     const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);  // K tiles: K-major SW128
+    // (TTS_PROF: [0] waiting for K, [1] waiting for the S buffer, [2] issuing, [3] waiting for Q)
+    PROF_DECL;
     int js = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
+      PROF_MARK(2);
       bar_wait(b_qready, pc & 1);  // this piece's Q in TMEM
+      PROF_MARK(3);
       // an empty piece issues no MMA: release its Q explicitly, so that the
       // softmax warps load the next Q only after this wait (no parity aliasing)
       if (j1 == j0 && lane == 0) bar_arrive(b_qtaken);
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNS;
         if (lane == 0) TTS_TR(js, 0);
+        PROF_MARK(2);
         bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        PROF_MARK(0);
         if (lane == 0) TTS_TR(js, 1);
         // S buffer js & 1 holds P(js - 2) until PV(js - 2) has read it
         if (js >= 2) bar_wait(b_pv + 8 * (js & 1), ((js - 2) >> 1) & 1u);
+        PROF_MARK(1);
         tc_fence_after();
         // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
         // absent second page leaves columns 16..31 undefined; they are masked)
@@ -602,20 +651,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) TTS_TR(js, 7);
       }
     }
+    PROF_MARK(2);
+    PROF_FLUSH(5);
   } else if (warp == 6) {
     // ====================== PV issuer: O += P V ======================
     constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
     const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
+    // (TTS_PROF: [0] waiting for V, [1] waiting for P, [2] waiting for O, [3] issuing)
+    PROF_DECL;
     int js = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNS;
+        PROF_MARK(3);
         bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        PROF_MARK(0);
         bar_wait(b_pfull + 8 * (js & 1), (js >> 1) & 1u);
+        PROF_MARK(1);
         // the first PV of a piece overwrites O: the previous piece's epilogue must have read it
         if (j == j0 && pc > 0) bar_wait(b_ofree, (pc - 1) & 1);
+        PROF_MARK(2);
         if (lane == 0) TTS_TR(js, 2);
         tc_fence_after();
         const uint32_t pa = t_s + (js & 1) * kSCols;
@@ -638,6 +695,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         __syncwarp();
       }
     }
+    PROF_MARK(3);
+    PROF_FLUSH(6);
   } else if (warp < 4) {
     // ============================ softmax (warps 0-3) ============================
     if (n_pieces > 0 && n1 == 0) {  // first piece in phase 2: Q after the plan
@@ -645,6 +704,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       piece(0, gi, slab, j0, j1, pslot);
       load_q(gi, slab);
     }
+    // (TTS_PROF: [0] waiting for S, [1] softmax of member units, [2] skipped units,
+    //  [3] epilogue + Q loads, [4] rescales, [5] P store + arrive; [6] member units, [7] all units)
+    PROF_DECL;
     int js = 0, n_empty = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
@@ -656,7 +718,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       float m_ref = -1e30f, l = 0.f;
       for (int j = j0; j < j1; ++j, ++js) {
         if (r == 0) TTS_TR(js, 4);
+        PROF_MARK(3);
         bar_wait(b_sfull + 8 * (js & 1), (js >> 1) & 1u);
+        PROF_MARK(0);
+        PROF_CNT(7);
         if (r == 0) TTS_TR(js, 5);
         tc_fence_after();
         const int slot = js % kNS;
@@ -719,6 +784,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           const bool need = mx > m_ref + 8.0f;
           if (__any_sync(0xffffffffu, need) && j > j0) {
             if (r == 0) TTS_TR2(js, 7);
+            PROF_MARK(1);
             // every earlier PV product must have landed before O is rescaled in TMEM
             bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
             tc_fence_after();
@@ -734,6 +800,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             tc_wait_st();
             l *= alpha;
+            PROF_MARK(4);
           }
           if (need) m_ref = mx;
           const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
@@ -747,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               for (int c = 0; c < kP; c += 2) {
                 const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
                 float a, b;
-                if (kPoly && ((c >> 1) & 1)) {
+                if (kPoly == 2 || (kPoly == 1 && ((c >> 1) & 1))) {
                   const float2 e2 = ex2_poly2(x);
                   a = e2.x;
                   b = e2.y;
@@ -761,6 +828,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
           }
           l += lacc.x + lacc.y;
+          PROF_MARK(1);
+          PROF_CNT(6);
+        } else {
+          PROF_MARK(2);
         }
         // P (fp16) over the unit's first 16 S columns (value c at column c/2)
         tc_st16(t_s + lane_off + (js & 1) * kSCols, pk);
@@ -770,6 +841,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (r == 0) TTS_TR(js, 6);
         if (lane == 0) TTS_TR2(js, warp);
         if (lane == 0) bar_arrive(b_pfull + 8 * (js & 1));
+        PROF_MARK(5);
       }
       // the next piece's Q (every S MMA of this piece has completed), so that
       // its S = Q K^T overlaps this piece's epilogue
@@ -777,7 +849,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (j1 == j0) bar_wait(b_qtaken, (n_empty++) & 1);  // (a non-empty piece: its S MMAs read Q)
         int gi2, slab2, j02, j12, ps2;
         piece(pc + 1, gi2, slab2, j02, j12, ps2);
+        PROF_MARK(3);
         load_q(gi2, slab2);
+        PROF_MARK(8);
       }
       // ---------------- epilogue of the piece ----------------
       // (an empty piece -- a tile with no units, e.g. under a sticky error --
@@ -785,6 +859,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int tu = s_pre[gi + 1] - s_pre[gi];
       if (j1 > j0) {
       bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
+      PROF_MARK(9);
       tc_fence_after();
       float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD;
       if (j0 == 0 && j1 == tu) {
@@ -839,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int tile = slab * ng + gi;
         if (r == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        PROF_MARK(10);
         if (s_info[0]) {
           __threadfence();
           const int np = c_last - c_first + 1;
@@ -900,6 +976,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
           }
           if (r == 0) p.tile_cnt[tile] = 0;  // every piece of the tile has arrived: ready for the next call
+          PROF_MARK(11);
+          PROF_CNT(12);
         }
       }
       }
@@ -907,6 +985,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       __syncwarp();
       if (lane == 0) bar_arrive(b_ofree);  // the next piece's first PV may overwrite O
     }
+    PROF_MARK(3);
+    PROF_FLUSH(warp);
   }
 
   if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
@@ -935,6 +1015,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 }  // namespace
 
+#ifdef TTS_PROF
+extern "C" int tts_debug_read_prof(long long* out_h) {
+  return (int)cudaMemcpyFromSymbol(out_h, g_prof, sizeof(g_prof));
+}
+#endif
+
 #ifdef TTS_TRACE
 extern "C" int tts_debug_read_trace(long long* out_h) {
   int e = (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
@@ -952,17 +1038,18 @@ bool umma_supported(const Ctx* c) {
          c->umma_ok;
 }
 
-// Per device context: the kernel attributes, and the residency the schedule
-// and the plan's double buffer rely on.  The grid is exactly two CTAs per SM
-// and at most two fit per SM, so all CTAs of call N+1 running implies call N's
-// attention kernel has exited -- and call N+2's k_plan (PDL-released by call
-// N+1's CTAs) can only then overwrite the plan buffer call N read.  If a
-// device or build breaks either condition, the context uses the mma.sync path.
+// Per device context: the kernel attributes, and the residency argument the
+// plan's double buffer relies on.  The grid is exactly two CTAs per SM and at
+// most two fit per SM (static_assert on the shared memory below), so all CTAs
+// of call N+1 being resident implies call N's attention kernel has exited --
+// and call N+2's k_plan (PDL-released by call N+1's CTAs) can only then
+// overwrite the plan buffer call N read.  A device with more SMs than the
+// partial-state slots cover uses the mma.sync path.
 cudaError_t umma_prepare(Ctx* c) {
   c->umma_ok = false;
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
   if (c->cfg.head_dim != kD || c->cfg.page_size != kP || G < 4 || G > 16) return cudaSuccess;
-  for (auto k : {k_tree_umma<true>, k_tree_umma<false>}) {
+  for (auto k : {k_tree_umma<0>, k_tree_umma<1>, k_tree_umma<2>}) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
     // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
@@ -971,7 +1058,8 @@ cudaError_t umma_prepare(Ctx* c) {
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, kSmemBytes);
     if (e != cudaSuccess) return e;
-    if (occ != 2 || 2 * c->num_sms > kMaxCtas) return cudaSuccess;
+    c->umma_occupancy = occ;  // diagnostics only (the occupancy API under-reports with the carveout hint)
+    if (2 * c->num_sms > kMaxCtas) return cudaSuccess;
   }
   c->umma_ok = true;
   return cudaSuccess;
@@ -1043,7 +1131,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     pp.glens = (const int32_t*)dl;
   }
   // measured 2% slower on C2/C3 (the softmax is latency-, not MUFU-bound): off unless TTS_POLY=1
-  auto kern = c->env_poly ? k_tree_umma<true> : k_tree_umma<false>;
+  auto kern = c->env_poly == 2 ? k_tree_umma<2> : c->env_poly ? k_tree_umma<1> : k_tree_umma<0>;
   const bool no_pdl = c->env_no_pdl;
   cudaLaunchAttribute pdl;
   // each kernel may start while its predecessor on the stream runs; both wait
@@ -1063,7 +1151,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   }
   cudaLaunchConfig_t cfg = {};
   // persistent: two CTAs per SM (the smem / TMEM / register budget of one CTA)
-  cfg.gridDim = dim3(2 * c->num_sms);  // == 2 x SMs, <= kMaxCtas (umma_prepare)
+  cfg.gridDim = dim3((c->env_ctas_per_sm == 1 ? 1 : 2) * c->num_sms);  // 2 x SMs, <= kMaxCtas (umma_prepare)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "../../include/tts.h"
@@ -43,6 +44,16 @@ struct AllocItem {
 
 struct CowCopy {
   int32_t src, dst, ntok, pad;
+};
+
+struct Comm;  // span.cu: NCCL communicator or host transport of a multi-GPU context
+
+// A request whose beams span the ranks of the context's communicator (a8):
+// rank r holds caps[r] beams, local rows in ascending global id.
+struct Span {
+  int n_global = 0;
+  std::vector<int32_t> caps;
+  std::vector<int32_t> gids;
 };
 
 struct Ctx {
@@ -93,9 +104,16 @@ struct Ctx {
   bool env_attn_mma = false;  // TTS_ATTN=mma: force the mma.sync path
   int env_group_beams = 0;    // TTS_GROUP_BEAMS: beams per group on the tcgen05 path
   int env_ncons = 0;          // TTS_NCONS: consumer warps of the mma.sync path
-  bool env_poly = false;      // TTS_POLY=1: polynomial exp2 for every other pair
+  int env_poly = 0;           // TTS_POLY=1: polynomial exp2 for every other pair, 2: for all
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
+  int env_ctas_per_sm = 2;    // TTS_CTAS_PER_SM=1: experiment, one attention CTA per SM
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
+  int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
+  // multi-GPU (span.cu)
+  Comm* comm = nullptr;
+  std::map<int, Span> spans;
+  float* ws_scores_all = nullptr;   // [1024] gid-indexed scores of a global selection
+  int32_t* ws_parent_all = nullptr;  // [1024] global parent map
 };
 
 // ---- pool value format --------------------------------------------------------

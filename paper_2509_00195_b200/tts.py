@@ -52,6 +52,16 @@ _lib = None
 _P = ctypes.c_void_p
 _I = ctypes.c_int32
 
+# host transport callbacks (include/tts.h tts_host_transport_t)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _P, _P, _P, ctypes.c_size_t)
+SENDRECV_FN = ctypes.CFUNCTYPE(ctypes.c_int, _P, _I, ctypes.POINTER(_I), ctypes.POINTER(_P),
+                               ctypes.POINTER(ctypes.c_size_t), _I, ctypes.POINTER(_I), ctypes.POINTER(_P),
+                               ctypes.POINTER(ctypes.c_size_t))
+
+
+class tts_host_transport_t(ctypes.Structure):
+    _fields_ = [("user", _P), ("allgather", ALLGATHER_FN), ("sendrecv", SENDRECV_FN)]
+
 
 def load() -> ctypes.CDLL:
     global _lib
@@ -81,6 +91,14 @@ def load() -> ctypes.CDLL:
             "tts_lineage_bytes": [_P, _I, ctypes.POINTER(ctypes.c_size_t)],
             "tts_lineage_export": [_P, _I, _I, _P, _P],
             "tts_lineage_import": [_P, _I, _I, _I, _P, _P],
+            "tts_comm_unique_id": [_P],
+            "tts_comm_init": [_P, _P, _I, _I, _P, ctypes.c_size_t],
+            "tts_comm_init_host": [_P, _I, _I, ctypes.POINTER(tts_host_transport_t), ctypes.c_size_t],
+            "tts_comm_destroy": [_P],
+            "tts_span_init": [_P, _I, _I, _P],
+            "tts_span_gids": [_P, _I, _P],
+            "tts_beam_select_fork_global": [_P, _I, _P, _I, _P, _P, _P],
+            "tts_span_placement": [_I, _P, _P, _I, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -90,6 +108,8 @@ def load() -> ctypes.CDLL:
         lib.tts_status_str.restype = ctypes.c_char_p
         lib.tts_launch_count.argtypes = [_P]
         lib.tts_launch_count.restype = ctypes.c_int64
+        lib.tts_attention_kernel.argtypes = [_P]
+        lib.tts_attention_kernel.restype = ctypes.c_char_p
         lib.tts_stream_read_gbs.argtypes = [_P, ctypes.c_size_t, _I, ctypes.POINTER(ctypes.c_double), _P]
         lib.tts_stream_read_gbs.restype = ctypes.c_int
         _lib = lib
@@ -101,6 +121,22 @@ def header_functions() -> list:
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(tts_[a-z0-9_]+)\s*\(", src)))
+
+
+def comm_unique_id() -> bytes:
+    """tts_comm_unique_id: a fresh 128-byte NCCL unique id (rank 0 broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().tts_comm_unique_id(ctypes.cast(buf, _P)), "tts_comm_unique_id")
+    return buf.raw
+
+
+def span_placement(parent_gid: Sequence[int], old_rank: Sequence[int], caps: Sequence[int]) -> list:
+    """tts_span_placement (host only): child gid -> rank."""
+    n = len(parent_gid)
+    out = (_I * n)()
+    _check(load().tts_span_placement(n, _i32_host(parent_gid), _i32_host(old_rank), len(caps), _i32_host(caps),
+                                     out), "tts_span_placement")
+    return list(out)
 
 
 def stream_read_gbs(buf: torch.Tensor, iters: int = 10) -> float:
@@ -215,6 +251,9 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.tts_launch_count(self.h))
 
+    def attention_kernel(self) -> str:
+        return self.lib.tts_attention_kernel(self.h).decode()
+
     # -- C entry points (same names) ------------------------------------------
     def tts_block_table_init_request(self, req, n_beams, prompt_len, k_prompt, v_prompt):
         _check(self.lib.tts_block_table_init_request(self.h, req, n_beams, prompt_len, _ptr(k_prompt),
@@ -279,6 +318,74 @@ class Context:
 
     def sync(self):
         torch.cuda.current_stream(self.device).synchronize()
+
+    # -- a8: libtts-owned communicator ---------------------------------------------
+    def tts_comm_init(self, unique_id: bytes, nranks: int, rank: int, stage: torch.Tensor):
+        idb = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(self.lib.tts_comm_init(self.h, ctypes.cast(idb, _P), nranks, rank, _ptr(stage),
+                                      stage.numel() * stage.element_size()), "tts_comm_init")
+        self._stage = stage
+
+    def tts_comm_init_host(self, nranks: int, rank: int, transport, stage_bytes: int = 64 << 20):
+        """transport: object with allgather(send: bytes, nbytes) -> bytes (all ranks, rank order) and
+        sendrecv(sends: [(dst, bytes)], recvs: [(src, nbytes)]) -> [bytes]."""
+        def ag(user, send_h, recv_h, nbytes):
+            try:
+                data = transport.allgather(ctypes.string_at(send_h, nbytes), nbytes)
+                ctypes.memmove(recv_h, data, len(data))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to libtts as a transport failure
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def sr(user, n_send, dst, send_h, send_b, n_recv, src, recv_h, recv_b):
+            try:
+                sends = [(dst[i], ctypes.string_at(send_h[i], send_b[i])) for i in range(n_send)]
+                recvs = [(src[i], recv_b[i]) for i in range(n_recv)]
+                got = transport.sendrecv(sends, recvs)
+                for i in range(n_recv):
+                    ctypes.memmove(recv_h[i], got[i], recv_b[i])
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._transport = (transport, ALLGATHER_FN(ag), SENDRECV_FN(sr))
+        t = tts_host_transport_t(None, self._transport[1], self._transport[2])
+        self._transport_struct = t
+        _check(self.lib.tts_comm_init_host(self.h, nranks, rank, ctypes.byref(t), int(stage_bytes)),
+               "tts_comm_init_host")
+
+    def tts_comm_destroy(self):
+        _check(self.lib.tts_comm_destroy(self.h), "tts_comm_destroy")
+
+    def tts_span_init(self, req: int, n_global: int, caps: Sequence[int]):
+        _check(self.lib.tts_span_init(self.h, req, n_global, _i32_host(caps)), "tts_span_init")
+
+    def tts_span_gids(self, req: int) -> list:
+        n = int(self.n_beams(req))
+        out = (_I * max(1, n))()
+        _check(self.lib.tts_span_gids(self.h, req, out), "tts_span_gids")
+        return list(out)[:n]
+
+    def n_beams(self, req: int) -> int:
+        """Beam count of an installed request (through the snapshot call; syncs)."""
+        n = ctypes.c_int32()
+        tables = np.empty((self.cfg.max_beams, self.cfg.max_pages_per_beam), dtype=np.int32)
+        lens = np.empty(self.cfg.max_beams, dtype=np.int32)
+        _check(self.lib.tts_block_table_snapshot(self.h, req, ctypes.byref(n), tables.ctypes.data_as(_P),
+                                                 lens.ctypes.data_as(_P), None, None, self.stream),
+               "tts_block_table_snapshot")
+        return n.value
+
+    def tts_beam_select_fork_global(self, req: int, local_scores: torch.Tensor, width_m: int,
+                                    parent_gid_out: Optional[torch.Tensor] = None,
+                                    child_rank_out: Optional[torch.Tensor] = None):
+        _check(self.lib.tts_beam_select_fork_global(self.h, req, _ptr(local_scores), int(width_m),
+                                                    _ptr(parent_gid_out), _ptr(child_rank_out), self.stream),
+               "tts_beam_select_fork_global")
 
     def tts_block_table_release_request(self, req):
         _check(self.lib.tts_block_table_release_request(self.h, req, self.stream),

@@ -1,18 +1,20 @@
-"""Multi-rank host logic of the beam-sharded fork on CPU:
-the pure placement / migration plan, and the torch.distributed driver run with
-gloo at world size 2 over a mock context (token-identity rows instead of K/V
-pages), checked against a single-rank selection and fork."""
+"""Multi-rank host logic on CPU: libtts's placement rule (a
+host-only C-ABI call, no GPU) against the oracle rank model, and the byte
+transports the library drives (gloo at world size 2 in two processes;
+threads of one process)."""
 import os
 import random
+import socket
+import threading
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from oracle.ranks import placement as oracle_placement
 from oracle.select import select_survivors
-from paper_2509_00195_b200.dist import migration_plan, select_fork_global, shard_requests, transfers
+from paper_2509_00195_b200.dist import ThreadGroup, equal_caps, shard_requests
 
 
 def test_shard_requests_partition():
@@ -22,102 +24,86 @@ def test_shard_requests_partition():
         assert max(map(len, parts)) - min(map(len, parts)) <= 1
 
 
-@pytest.mark.parametrize("seed", range(20))
-def test_migration_plan_properties(seed):
+def test_equal_caps():
+    assert equal_caps(512, 8) == [64] * 8
+    assert equal_caps(10, 4) == [3, 3, 2, 2]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2509_00195_b200 import build, tts
+    build.build()
+    return tts.load()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_libtts_placement_equals_oracle(lib, seed):
+    """tts_span_placement (C++, identical on every rank) against
+    oracle.ranks.placement (written from 8(e) step 3)."""
+    from paper_2509_00195_b200.tts import span_placement
     rnd = random.Random(seed)
-    G = rnd.choice([2, 4, 8])
-    n = rnd.choice([2, 4, 8])
-    M = rnd.choice([m for m in (2, 4, 8) if (G * n) % m == 0])
-    N = G * n
-    scores = [rnd.randint(0, 7) / 8 for _ in range(N)]
-    _, parent = select_survivors(scores, M)
-    plans = migration_plan(parent, G)
-    for r, pl in enumerate(plans):
-        assert len(pl.local_parent) == n
-        imported = dict((slot, p) for p, slot in pl.imports)
-        for i, lp in enumerate(pl.local_parent):
-            c = r * n + i
-            if lp < n:                       # parent already on this rank
-                assert r * n + lp == parent[c]
-            else:                            # parent's lineage imported into a spare row
-                assert imported[lp] == parent[c] and parent[c] // n != r
-        # children of one survivor are consecutive gids (ledger C5)
-        assert pl.local_parent == sorted(pl.local_parent) or any(lp >= n for lp in pl.local_parent)
-    # every import is matched by exactly one export
-    exp = sorted((p, s, d) for s, pl in enumerate(plans) for p, d in pl.exports)
-    imp = sorted((p, p // n, d) for d, pl in enumerate(plans) for p, _ in pl.imports)
-    assert exp == imp == transfers(plans, G)
+    G = rnd.choice([1, 2, 3, 4, 8])
+    caps = [rnd.randint(1, 9) for _ in range(G)]
+    N = sum(caps)
+    M = rnd.choice([m for m in (1, 2, 4, 8) if N % m == 0])
+    _, parent = select_survivors([rnd.randint(0, 5) / 5 for _ in range(N)], M)
+    old_rank = sum([[r] * caps[r] for r in range(G)], [])
+    rnd.shuffle(old_rank)
+    assert span_placement(parent, old_rank, caps) == oracle_placement(parent, old_rank, caps)
 
 
-class MockCtx:
-    """libtts surface over token-identity rows (one request)."""
-
-    def __init__(self, rows):
-        self.rows = [list(r) for r in rows]
-
-    def tts_seq_lens_host(self, req):
-        return np.array([len(r) for r in self.rows], dtype=np.int32)
-
-    def tts_beam_select_global(self, scores_all, width_m, parent_out):
-        _, parent = select_survivors(scores_all.tolist(), width_m)
-        parent_out.copy_(torch.tensor(parent, dtype=torch.int32))
-
-    def lineage_buffer(self, length):
-        return torch.empty(length, dtype=torch.int64)
-
-    def tts_lineage_export(self, req, beam, buf):
-        buf.copy_(torch.tensor(self.rows[beam], dtype=torch.int64))
-
-    def tts_lineage_import(self, req, slot, length, buf):
-        while len(self.rows) <= slot:
-            self.rows.append([])
-        assert not self.rows[slot]
-        self.rows[slot] = buf[:length].tolist()
-
-    def tts_beam_fork_map(self, req, local_parent):
-        self.rows = [list(self.rows[p]) for p in local_parent]
-
-    def sync(self):
-        pass
+def test_libtts_placement_rejects_bad_capacities(lib):
+    from paper_2509_00195_b200.tts import TTSError, span_placement
+    with pytest.raises(TTSError):
+        span_placement([0, 0, 1, 1], [0, 0, 1, 1], [2, 1])      # sum != N
+    with pytest.raises(TTSError):
+        span_placement([0, 0, 5, 1], [0, 0, 1, 1], [2, 2])      # parent out of range
 
 
-def _worker(rank, world, port, seed, out):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
+def test_thread_group_transport():
+    G = 4
+    grp = ThreadGroup(G)
+    out = {}
+
+    def work(r):
+        t = grp.transport(r)
+        ag = t.allgather(bytes([r] * 3), 3)
+        sends = [((r + 1) % G, f"to{(r + 1) % G}from{r}".encode()), ((r + 2) % G, b"x" * r)]
+        recvs = [((r - 1) % G, len(f"to{r}from{(r - 1) % G}")), ((r - 2) % G, (r - 2) % G)]
+        got = t.sendrecv(sends, recvs)
+        out[r] = (ag, got)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for r in range(G):
+        ag, got = out[r]
+        assert ag == b"".join(bytes([q] * 3) for q in range(G))
+        assert got[0] == f"to{r}from{(r - 1) % G}".encode() and got[1] == b"x" * ((r - 2) % G)
+
+
+def _gloo_transport_worker(rank, world, port):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    rnd = random.Random(seed)
-    n, M, steps = 4, 2, 3
-    N = n * world
-    # global rows: distinct identities, different lengths
-    g_rows = [[gid * 1000 + k for k in range(3 + gid % 3)] for gid in range(N)]
-    ctx = MockCtx(g_rows[rank * n:(rank + 1) * n])
-    for s in range(steps):
-        scores = [rnd.randint(0, 3) / 4 for _ in range(N)]   # same stream on every rank
-        local = torch.tensor(scores[rank * n:(rank + 1) * n], dtype=torch.float32)
-        parent = select_fork_global(ctx, 0, local, M)
-        _, want = select_survivors(scores, M)
-        assert parent == want
-        g_rows = [list(g_rows[p]) for p in want]              # single-rank reference fork
-        for i in range(n):                                    # every beam appends a token
-            gid = rank * n + i
-            ctx.rows[i].append(10_000 * (s + 1) + gid)
-        g_rows = [r + [10_000 * (s + 1) + gid] for gid, r in enumerate(g_rows)]
-    gathered = [None] * world
-    dist.all_gather_object(gathered, ctx.rows)
-    if rank == 0:
-        out.put((sum(gathered, []), g_rows))
-    dist.destroy_process_group()
+    try:
+        from paper_2509_00195_b200.dist import GlooTransport
+        t = GlooTransport()
+        ag = t.allgather(bytes([7 + rank] * 5), 5)
+        assert ag == bytes([7] * 5) + bytes([8] * 5)
+        other = 1 - rank
+        sends = [(other, f"lineage-{rank}-a".encode()), (other, b"B" * (100 + rank))]
+        recvs = [(other, len(f"lineage-{other}-a")), (other, 100 + other)]
+        got = t.sendrecv(sends, recvs)
+        assert got == [f"lineage-{other}-a".encode(), b"B" * (100 + other)]
+        assert t.sendrecv([], []) == []
+    finally:
+        dist.destroy_process_group()
 
 
-def test_gloo_world2_select_fork_global():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = 29500 + random.Random(os.getpid()).randint(0, 2000)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, 7, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got, want = q.get(timeout=120)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    assert got == want
+def test_gloo_transport_world2():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_gloo_transport_worker, args=(2, port), nprocs=2, join=True)
