@@ -204,6 +204,26 @@ tts_status_t tts_beam_select_fork(tts_ctx_t ctx, int32_t n_req, const int32_t* r
                                   const float* scores, int32_t width_m, int32_t* parent_out,
                                   void* stream);
 
+/* f2. Selection variants (DESIGN.md
+ * ledger C23/C24).  Same call shape and fork rules as tts_beam_select_fork;
+ * the parent map comes from:
+ *   TTS_SELECT_TOPK     beam search, param = M (K = N/M survivors x M children);
+ *   TTS_SELECT_DIVERSE  diverse selection (DVTS), param = B subtrees: subtree s
+ *                       is beams [s N/B, (s+1) N/B) (DFS order); its best beam
+ *                       spawns the N/B children of subtree s;
+ *   TTS_SELECT_DYNAMIC  dynamic branching, param = M: the K = N/M beam-search
+ *                       survivors get 1 + floor(q_i) children, q_i =
+ *                       (N - K) w_i / sum(w) in fp64 (w = score if finite and
+ *                       > 0, else 0; all 0 -> equal), the remaining children
+ *                       by largest fractional part (ties: lower index).
+ * Children of a survivor are contiguous, in survivor (index) order; every
+ * child but the first of its parent copies a partially filled last page.
+ * Errors: TTS_ERR_INVALID_ARG if N % param != 0 or the policy is unknown. */
+enum { TTS_SELECT_TOPK = 0, TTS_SELECT_DIVERSE = 1, TTS_SELECT_DYNAMIC = 2 };
+tts_status_t tts_beam_select_fork_policy(tts_ctx_t ctx, int32_t n_req, const int32_t* req_ids_h,
+                                         const float* scores, int32_t policy, int32_t param,
+                                         int32_t* parent_out, void* stream);
+
 /* ---- a8: one request's beams spanning G GPUs --------------
  * The request's N_global beams are held in G contiguous ranges of global ids
  * (gid = rank * N_local + local index; DFS order across ranks).  Per step:

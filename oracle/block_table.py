@@ -154,6 +154,45 @@ class BlockTableSim:
             self.lens[r] = lens
         return parents
 
+    def fork_parents(self, reqs: Sequence[int], parents: Sequence[Sequence[int]]) -> None:
+        """Fork by explicit parent maps (selection variants): new
+        row c = old row parents[c]; releases before allocations (C7); eager CoW
+        of a partially filled last page for every child that is not the first
+        child of its parent (children of a parent are contiguous, C5; for
+        beam search this is child j = c mod M >= 1, C6)."""
+        P = self.P
+        new_tables, new_lens = {}, {}
+        for k, r in enumerate(reqs):
+            par = parents[k]
+            new_tables[r] = [list(self.tables[r][par[c]]) for c in range(len(par))]
+            new_lens[r] = [self.lens[r][par[c]] for c in range(len(par))]
+        touched = set()
+        for r in reqs:
+            for row in self.tables[r]:
+                for p in row:
+                    self.ref[p] -= 1
+                    touched.add(p)
+            for row in new_tables[r]:
+                for p in row:
+                    self.ref[p] += 1
+        for p in sorted(touched):
+            if self.ref[p] == 0:
+                self._release(p)
+        for k, r in enumerate(reqs):
+            par = parents[k]
+            rows, lens = new_tables[r], new_lens[r]
+            for c in range(len(rows)):
+                rem = lens[c] % P
+                if c > 0 and par[c] == par[c - 1] and rem != 0:
+                    src = rows[c][-1]
+                    newp = self._alloc()
+                    self._copy_tokens(newp, src, rem)
+                    rows[c][-1] = newp
+                    self.ref[src] -= 1
+                    self.ref[newp] = 1
+            self.tables[r] = rows
+            self.lens[r] = lens
+
     def release_request(self, req: int) -> None:
         for row in self.tables.pop(req):
             for p in row:

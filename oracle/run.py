@@ -30,7 +30,7 @@ import torch
 from synth import rng, workload
 from .attention import attention_fp64
 from .block_table import BlockTableSim
-from .select import select_survivors
+from .select import select_policy, select_survivors
 
 
 def default_num_pages(cfg: workload.Config, n_req: int) -> int:
@@ -135,7 +135,10 @@ class OracleRun:
     def run(self, sample: Optional[Callable[[workload.Iteration], List[Tuple[int, int, int]]]] = None,
             snapshot_refs: bool = True, stats: bool = False, max_iters: Optional[int] = None,
             scores_fn: Optional[Callable[[int, int], Sequence[float]]] = None,
-            on_fork: Optional[Callable[["OracleRun", ForkRecord], None]] = None) -> Trace:
+            on_fork: Optional[Callable[["OracleRun", ForkRecord], None]] = None,
+            policy: Optional[Tuple[int, int]] = None) -> Trace:
+        """policy: (select.POLICY_*, param) for the selection variants (f2); default
+        beam search with the configuration's M."""
         c = self.cfg
         tr = Trace()
         self.install()
@@ -165,11 +168,16 @@ class OracleRun:
                 for r, s in it.forks:
                     sc = scores_fn(r, s) if scores_fn else workload.scores(c, r, s).tolist()
                     scs.append(list(sc))
-                parents = self.sim.fork(reqs, scs, c.M)
+                if policy is None:
+                    parents = self.sim.fork(reqs, scs, c.M)
+                else:
+                    parents = [select_policy(sc, policy[0], policy[1]) for sc in scs]
+                    self.sim.fork_parents(reqs, parents)
                 rec = ForkRecord(t=it.t, reqs=reqs, parents={}, tables={}, lens={})
                 for k, r in enumerate(reqs):
-                    _, parent = select_survivors(scs[k], c.M)
-                    assert parent == parents[k]
+                    parent = parents[k]
+                    if policy is None:
+                        assert parent == select_survivors(scs[k], c.M)[1]
                     self.lists[r] = [self.lists[r][parent[cc]].copy() for cc in range(c.N)]
                     rec.parents[r] = parent
                     rec.tables[r] = [list(row) for row in self.sim.tables[r]]

@@ -185,7 +185,7 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_NCONS")) c->env_ncons = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::max(0, std::min(2, std::atoi(s)));
   c->env_no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
-  if (const char* s = std::getenv("TTS_CTAS_PER_SM")) c->env_ctas_per_sm = std::atoi(s) == 1 ? 1 : 2;
+  if (const char* s = std::getenv("TTS_S_AHEAD")) c->env_s_ahead = std::atoi(s);
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
@@ -413,15 +413,12 @@ static tts_status_t attn_prepare(tts_ctx_t c, int32_t layer_begin, int32_t layer
   if (ap.umma) {
     // 128-row tiles: balanced runs of <= umma_max_beams beams of one request.
     // The largest groups (a page shared inside a group is staged once) that
-    // still give >= 3/4 of a round of tiles for the 2 CTAs per SM of the
-    // persistent kernel; a smaller remainder is split over all CTAs there
-    // (stream-K).  Measured (C2, one request per call): 4-beam groups, 224
-    // whole tiles, 40 us per call vs 16-beam groups, 56 tiles split ~5 ways,
-    // 59 us (the split pieces cost unequal time: the shared prefix at the head
-    // of a tile keeps all four softmax warps busy, a private tail one).
+    // still give >= 3/4 of a round of tiles for the CTAs of the persistent
+    // kernel (one per SM); a smaller remainder is split over all CTAs there
+    // (stream-K).
     int maxb = tts::umma_max_beams(c);
     if (c->env_group_beams) maxb = std::max(1, std::min(maxb, c->env_group_beams));
-    const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;
+    const int64_t want = (3ll * c->num_sms + 3) / 4;
     auto group_size = [&](int cap) {
       int gb = 1;
       for (int i = 0; i < n_req; ++i) {
@@ -576,9 +573,8 @@ tts_status_t tts_profile_end(tts_ctx_t c, double* ms, int64_t* n) {
   return TTS_OK;
 }
 
-tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
-                                  const float* scores, int32_t M, int32_t* parent_out,
-                                  void* stream) {
+static tts_status_t select_fork_impl(tts_ctx_t c, int32_t n_req, const int32_t* req_ids, const float* scores,
+                                     int32_t policy, int32_t param, int32_t* parent_out, void* stream) {
   if (!c || n_req <= 0 || !req_ids || !scores) return TTS_ERR_INVALID_ARG;
   const tts_config_t& g = c->cfg;
   for (int i = 0; i < n_req; ++i)
@@ -586,7 +582,8 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   const int N = c->n_beams[req_ids[0]];
   for (int i = 0; i < n_req; ++i)
     if (c->n_beams[req_ids[i]] != N) return TTS_ERR_INVALID_ARG;
-  if (M <= 0 || N % M) return TTS_ERR_INVALID_ARG;
+  if (policy < TTS_SELECT_TOPK || policy > TTS_SELECT_DYNAMIC) return TTS_ERR_INVALID_ARG;
+  if (param <= 0 || N % param) return TTS_ERR_INVALID_ARG;  // N % M (top-K, dynamic), N % B (diverse)
   for (int i = 0; i < n_req; ++i)
     for (int j = 0; j < i; ++j)
       if (req_ids[i] == req_ids[j]) return TTS_ERR_INVALID_ARG;
@@ -596,7 +593,10 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   cudaError_t e;
   void* dreq = tts::upload(c, req_ids, (size_t)n_req * 4, st, &e);
   TTS_CUDA(e);
-  TTS_CUDA(tts::launch_select(c, (const int32_t*)dreq, n_req, scores, N, M, parent_out, st));
+  if (policy == TTS_SELECT_TOPK)
+    TTS_CUDA(tts::launch_select(c, (const int32_t*)dreq, n_req, scores, N, param, parent_out, st));
+  else
+    TTS_CUDA(tts::launch_select_policy(c, n_req, scores, N, policy, param, parent_out, st));
   TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, n_req, N, N, st));
   // parent map back to the host (for the length mirror and the CoW plan)
   std::vector<int32_t> parent((size_t)n_req * g.max_beams);
@@ -606,16 +606,18 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
   std::vector<tts::AllocItem> items;
   for (int i = 0; i < n_req; ++i) {
     const int r = req_ids[i];
+    const int32_t* par = parent.data() + (int64_t)i * g.max_beams;
     int32_t* lens = c->lens.data() + (int64_t)r * g.max_beams;
     std::vector<int32_t> old(lens, lens + N);
     for (int cc = 0; cc < N; ++cc) {
-      const int par = parent[(int64_t)i * g.max_beams + cc];
-      if (par < 0 || par >= N) return TTS_ERR_STATE;  // sticky device error upstream
-      lens[cc] = old[par];
+      if (par[cc] < 0 || par[cc] >= N) return TTS_ERR_STATE;  // sticky device error upstream
+      lens[cc] = old[par[cc]];
     }
-    for (int cc = 0; cc < N; ++cc) {
+    // eager CoW (ledger C6): every child but the first of its parent (children
+    // of a parent are contiguous) copies a partially filled last page
+    for (int cc = 1; cc < N; ++cc) {
       const int len = lens[cc];
-      if (cc % M >= 1 && len % P) items.push_back({entry_of(g, r, cc, (len - 1) / P), 1, len % P});
+      if (par[cc] == par[cc - 1] && len % P) items.push_back({entry_of(g, r, cc, (len - 1) / P), 1, len % P});
     }
   }
   if (!items.empty()) {
@@ -623,6 +625,16 @@ tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req
     TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
   }
   return TTS_OK;
+}
+
+tts_status_t tts_beam_select_fork(tts_ctx_t c, int32_t n_req, const int32_t* req_ids, const float* scores,
+                                  int32_t M, int32_t* parent_out, void* stream) {
+  return select_fork_impl(c, n_req, req_ids, scores, TTS_SELECT_TOPK, M, parent_out, stream);
+}
+
+tts_status_t tts_beam_select_fork_policy(tts_ctx_t c, int32_t n_req, const int32_t* req_ids, const float* scores,
+                                         int32_t policy, int32_t param, int32_t* parent_out, void* stream) {
+  return select_fork_impl(c, n_req, req_ids, scores, policy, param, parent_out, stream);
 }
 
 // CoW plan of a fork by parent map: the first child (in index order) of each

@@ -280,6 +280,110 @@ __global__ void __launch_bounds__(kSelThreads) k_select(DevState s, const int32_
   (void)reqs;
 }
 
+// Selection variants (ledger C23/C24): one CTA per request.
+//   policy 1, diverse (DVTS): subtree s = beams [s n, (s+1) n), n = N / param;
+//     its best beam (the orderable key above) spawns the n children of subtree s.
+//   policy 2, dynamic branching: the K = N / param survivors of beam search,
+//     child counts 1 + floor(q_i) + (largest-remainder extra), q_i = (N - K)
+//     w_i / sum(w) in fp64 (the sum in survivor order, by one thread, the way
+//     the oracle adds), w = score if finite and > 0 else 0 (all 0 -> equal).
+// parent_ws / parent_out as k_select.
+__global__ void __launch_bounds__(kSelThreads) k_select_policy(DevState s, const float* scores, int N, int policy,
+                                                               int param, int32_t* parent_ws, int32_t* parent_out) {
+  using Scan = cub::BlockScan<int, kSelThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint64_t keys[1024];
+  __shared__ int32_t surv[1024];
+  __shared__ int32_t cnt[1024];
+  __shared__ double frac[1024];
+  __shared__ double wsum;
+  if (*(volatile int32_t*)s.status) return;
+  const int call = blockIdx.x;
+  const int tid = threadIdx.x;
+  uint64_t my = 0;
+  if (tid < N) {
+    my = order_key(scores[(int64_t)call * s.maxB + tid], tid);
+    keys[tid] = my;
+  }
+  __syncthreads();
+  int32_t par = 0;
+  if (policy == 1) {
+    const int n = N / param;
+    if (tid < param) {  // one thread per subtree: its best beam
+      int best = tid * n;
+      for (int i = tid * n + 1; i < (tid + 1) * n; ++i)
+        if (keys[i] > keys[best]) best = i;
+      surv[tid] = best;
+    }
+    __syncthreads();
+    if (tid < N) par = surv[tid / n];
+  } else {
+    const int K = N / param;
+    int flag = 0;
+    if (tid < N) {
+      int rank = 0;
+      for (int j = 0; j < N; ++j) rank += keys[j] > my;
+      flag = rank < K;
+    }
+    int pos;
+    Scan(tmp).ExclusiveSum(flag, pos);
+    if (flag) surv[pos] = tid;
+    __syncthreads();
+    if (tid == 0) {
+      double w = 0.0;
+      for (int i = 0; i < K; ++i) {
+        const double x = (double)scores[(int64_t)call * s.maxB + surv[i]];
+        w += (isfinite(x) && x > 0.0) ? x : 0.0;
+      }
+      wsum = w;
+    }
+    __syncthreads();
+    int c = 0;
+    if (tid < K) {
+      const double x = (double)scores[(int64_t)call * s.maxB + surv[tid]];
+      double wi = (isfinite(x) && x > 0.0) ? x : 0.0, W = wsum;
+      if (W == 0.0) {
+        wi = 1.0;
+        W = (double)K;
+      }
+      const double q = __dmul_rn((double)(N - K), wi);
+      const double qq = __ddiv_rn(q, W);
+      const double fl = floor(qq);
+      c = 1 + (int)fl;
+      frac[tid] = qq - fl;
+      cnt[tid] = c;
+    }
+    int csum;
+    {
+      int tot;
+      Scan(tmp).ExclusiveSum(c, csum, tot);
+      __syncthreads();
+      if (tid == 0) wsum = (double)(N - tot);  // children still to place
+    }
+    __syncthreads();
+    const int rest = (int)wsum;
+    if (tid < K) {  // rank by (fraction desc, survivor index asc)
+      int rank = 0;
+      const double f = frac[tid];
+      for (int j = 0; j < K; ++j) rank += frac[j] > f || (frac[j] == f && j < tid);
+      if (rank < rest) cnt[tid] = c + 1;
+    }
+    __syncthreads();
+    int off, c2 = tid < K ? cnt[tid] : 0;
+    Scan(tmp).ExclusiveSum(c2, off);
+    if (tid < K)
+      for (int k = 0; k < c2; ++k) {
+        parent_ws[(int64_t)call * s.maxB + off + k] = surv[tid];
+        if (parent_out) parent_out[(int64_t)call * s.maxB + off + k] = surv[tid];
+      }
+    return;
+  }
+  if (tid < N) {
+    parent_ws[(int64_t)call * s.maxB + tid] = par;
+    if (parent_out) parent_out[(int64_t)call * s.maxB + tid] = par;
+  }
+}
+
 // Fork, step A: new rows into tmp (child c <- old row parent[c]); refcounts
 // recounted by -1 per old-row entry and +1 per new-row entry (commuting
 // atomics).  Old rows [0, n_old), new rows [0, n_new); n_old > n_new when
@@ -520,6 +624,13 @@ cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float*
                           int M, int32_t* parent_out, cudaStream_t st) {
   k_select<<<n_req, kSelThreads, 0, st>>>(dev_state(c), reqs_d, scores, N, M, c->ws_parent,
                                           parent_out);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_policy(Ctx* c, int n_req, const float* scores, int N, int policy, int param,
+                                 int32_t* parent_out, cudaStream_t st) {
+  k_select_policy<<<n_req, kSelThreads, 0, st>>>(dev_state(c), scores, N, policy, param, c->ws_parent, parent_out);
   c->launches++;
   return cudaGetLastError();
 }

@@ -106,8 +106,8 @@ struct Ctx {
   int env_ncons = 0;          // TTS_NCONS: consumer warps of the mma.sync path
   int env_poly = 0;           // TTS_POLY=1: polynomial exp2 for every other pair, 2: for all
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
-  int env_ctas_per_sm = 2;    // TTS_CTAS_PER_SM=1: experiment, one attention CTA per SM
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
+  int env_s_ahead = 0;        // TTS_S_AHEAD: S run-ahead of the tcgen05 kernel (units, <= 6)
   int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
   // multi-GPU (span.cu)
   Comm* comm = nullptr;
@@ -163,6 +163,8 @@ cudaError_t launch_append_write(Ctx* c, const int32_t* slots_d, int n_slots, int
                                 const __nv_bfloat16* k, const __nv_bfloat16* v, cudaStream_t s);
 cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float* scores,
                           int N, int M, int32_t* parent_out, cudaStream_t s);
+cudaError_t launch_select_policy(Ctx* c, int n_req, const float* scores, int N, int policy, int param,
+                                 int32_t* parent_out, cudaStream_t s);
 cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t s);
 cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t s);
 cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t s);

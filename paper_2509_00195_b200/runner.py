@@ -116,9 +116,10 @@ class BeamStepRunner:
             self.ctx.tts_block_table_release_request(self.local[r])
 
     def run(self, on_iter: Optional[Callable] = None, on_fork: Optional[Callable] = None,
-            max_iters: Optional[int] = None, scores_fn: Optional[Callable] = None) -> int:
+            max_iters: Optional[int] = None, scores_fn: Optional[Callable] = None, policy=None) -> int:
         """Whole run; returns beam-steps.  on_iter(it, out, q) after attention;
-        on_fork(it, parents {greq: np.ndarray}) after each fork."""
+        on_fork(it, parents {greq: np.ndarray}) after each fork.  policy:
+        (tts.SELECT_*, param) for the selection variants (default beam search, M)."""
         c = self.cfg
         self.install()
         beam_steps = 0
@@ -146,7 +147,11 @@ class BeamStepRunner:
                 else:
                     sc = torch.stack([self.inputs.scores(r, s) for r, s in it.forks])
                 parent = torch.empty(len(greqs), c.N, dtype=torch.int32, device=self.dev)
-                self.ctx.tts_beam_select_fork([self.local[r] for r in greqs], sc.contiguous(), c.M, parent)
+                if policy is None:
+                    self.ctx.tts_beam_select_fork([self.local[r] for r in greqs], sc.contiguous(), c.M, parent)
+                else:
+                    self.ctx.tts_beam_select_fork_policy([self.local[r] for r in greqs], sc.contiguous(), policy[0],
+                                                         policy[1], parent)
                 if on_fork is not None:
                     on_fork(it, {r: parent[i].cpu().numpy() for i, r in enumerate(greqs)})
         return beam_steps

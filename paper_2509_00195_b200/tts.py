@@ -21,6 +21,9 @@ LIB_PATH = os.environ.get("TTS_LIB_PATH") or os.path.join(HERE, "libtts.so")  # 
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tts.h")
 
 
+SELECT_TOPK, SELECT_DIVERSE, SELECT_DYNAMIC = 0, 1, 2  # include/tts.h
+
+
 class TTSError(RuntimeError):
     def __init__(self, code: int, what: str = ""):
         self.code = code
@@ -79,6 +82,7 @@ def load() -> ctypes.CDLL:
             "tts_block_table_append": [_P, _I, _P, _P, _P, _P, _P],
             "tts_prefix_attn_decode": [_P, _I, _I, _I, _P, _P, _P, ctypes.c_float, _P, _P],
             "tts_beam_select_fork": [_P, _I, _P, _P, _I, _P, _P],
+            "tts_beam_select_fork_policy": [_P, _I, _P, _P, _I, _I, _P, _P],
             "tts_block_table_release_request": [_P, _I, _P],
             "tts_block_table_snapshot": [_P, _I, _P, _P, _P, _P, _P, _P],
             "tts_block_table_stats": [_P, _I, _P, _P, _P, _P],
@@ -292,6 +296,11 @@ class Context:
         _check(self.lib.tts_beam_select_fork(self.h, len(req_ids), _i32_host(req_ids), _ptr(scores),
                                              int(width_m), _ptr(parent_out), self.stream),
                "tts_beam_select_fork")
+
+    def tts_beam_select_fork_policy(self, req_ids, scores, policy, param, parent_out=None):
+        _check(self.lib.tts_beam_select_fork_policy(self.h, len(req_ids), _i32_host(req_ids), _ptr(scores),
+                                                    int(policy), int(param), _ptr(parent_out), self.stream),
+               "tts_beam_select_fork_policy")
 
     def tts_beam_select_global(self, scores_all, width_m, parent_gid_out):
         _check(self.lib.tts_beam_select_global(self.h, scores_all.numel(), _ptr(scores_all), int(width_m),

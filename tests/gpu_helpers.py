@@ -36,12 +36,12 @@ def compare_state(snap: dict, tables: List[List[int]], lens: List[int], P: int,
 
 def run_parity(cfg: workload.Config, sample: Callable, num_pages: Optional[int] = None,
                scores_fn: Optional[Callable] = None, max_iters: Optional[int] = None,
-               check_refs: bool = True, fused: bool = True) -> Dict[str, float]:
+               check_refs: bool = True, fused: bool = True, policy=None) -> Dict[str, float]:
     from paper_2509_00195_b200.runner import BeamStepRunner
 
     num_pages = num_pages or default_num_pages(cfg, cfg.R)
     orc = OracleRun(cfg, num_pages=num_pages, track_content=cfg.R * cfg.N <= 64)
-    tr = orc.run(sample=sample, snapshot_refs=check_refs, scores_fn=scores_fn, max_iters=max_iters)
+    tr = orc.run(sample=sample, snapshot_refs=check_refs, scores_fn=scores_fn, max_iters=max_iters, policy=policy)
 
     runner = BeamStepRunner(cfg, num_pages=num_pages, fused=fused)
     ctx = runner.ctx
@@ -61,7 +61,7 @@ def run_parity(cfg: workload.Config, sample: Callable, num_pages: Optional[int] 
             rec["snap"][r] = ctx.tts_block_table_snapshot(runner.local[r], with_pool_state=check_refs)
         snaps.append(rec)
 
-    steps = runner.run(on_iter=on_iter, on_fork=on_fork, max_iters=max_iters, scores_fn=scores_fn)
+    steps = runner.run(on_iter=on_iter, on_fork=on_fork, max_iters=max_iters, scores_fn=scores_fn, policy=policy)
     assert ctx.tts_device_status() == 0
     assert steps == tr.beam_steps
 

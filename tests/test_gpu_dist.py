@@ -175,7 +175,7 @@ def test_nccl_one_rank_communicator():
     _span_run(cfg, [16], "nccl1")
 
 
-def _gloo_worker(rank, world, port, q):
+def _gloo_worker(rank, world, port, queue):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -212,7 +212,7 @@ def _gloo_worker(rank, world, port, q):
                                          for b, ln in enumerate(snap["lens"])],
                               "ref": snap["ref"].tolist(), "free": snap["free"].tolist()})
         assert ctx.tts_device_status() == 0
-        q.put((rank, snaps, cfg, caps))
+        queue.put((rank, snaps, cfg, caps))
     finally:
         dist.destroy_process_group()
 

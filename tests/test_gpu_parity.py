@@ -149,3 +149,23 @@ def test_outputs_bit_identical_across_runs(name, cfg):
     assert len(a) == len(b) > 0
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("policy,param,seed", [(1, 2, 0), (1, 4, 1), (2, 2, 2), (2, 4, 3), (1, 8, 4), (2, 8, 5)])
+def test_selection_variants(policy, param, seed):
+    """f2: diverse selection (policy 1, param = B subtrees) and dynamic
+    branching (policy 2, param = M) -- parent maps, tables, refcounts and free
+    sets bit-exact against the oracle at every fork, attention within 2e-3."""
+    rnd = random.Random(900 + seed)
+    d, G = rnd.choice([(128, 6), (128, 7), (64, 2)])
+    cfg = workload.Config(f"sel{policy}-{param}", R=rnd.choice([1, 2]), N=16, M=4, L=2, Hq=2 * G, Hkv=2, d=d, P=16,
+                          prompt=rnd.choice([0, 21, 32]), n_steps=4, step_len=0, ln_mu=math.log(15), ln_sigma=1.0,
+                          ln_cap=40, seed=8800 + seed, fine_scores=seed % 2 == 1)
+    run_parity(cfg, all_beams(cfg, every=4), policy=(policy, param))
+
+
+def test_selection_dynamic_c1_tie_scores():
+    # C1 shape with the scores of the SURVEY 8(c) trace, dynamic branching M = 2
+    cfg = workload.C1.with_(n_steps=4)
+    table = {0: [0.9, 0.1, 0.5, 0.5], 1: [0.5, 0.75, 0.75, 0.75], 2: [0.8, 0.2, 0.0, float("nan")]}
+    run_parity(cfg, all_beams(cfg, 5), scores_fn=lambda r, s: table[s], policy=(2, 2))

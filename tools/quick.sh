@@ -1,11 +1,13 @@
 #!/bin/bash
-# quick GPU iteration: profile split (TTS_PROF), C3 + C2 bench lines, a parity subset
+# quick GPU iteration: parity subset first (a broken kernel stops here), then the
+# profile split (TTS_PROF) and the C3 + C2 bench lines
 tag=${1:-q}
 mkdir -p gpurun_out
 python -c "from paper_2509_00195_b200 import build; build.build(force=True)" > gpurun_out/${tag}_build.log 2>&1
-python tools/prof.py C3 3 > gpurun_out/${tag}_prof_c3.log 2>&1
-python tools/prof.py C2 3 > gpurun_out/${tag}_prof_c2.log 2>&1
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${tag}_bench_C3.json 2> gpurun_out/${tag}_bench_C3.err
-python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${tag}_bench_C2.json 2> gpurun_out/${tag}_bench_C2.err
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "c3_full or random_small or split or hybrid or c1_full" > gpurun_out/${tag}_tests.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c1_full or random_small or split or hybrid or selection or c3_full" > gpurun_out/${tag}_tests.log 2>&1
+echo "pytest exit $?" >> gpurun_out/${tag}_tests.log
+timeout 300 python tools/prof.py C3 3 > gpurun_out/${tag}_prof_c3.log 2>&1
+timeout 300 python tools/prof.py C2 3 > gpurun_out/${tag}_prof_c2.log 2>&1
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${tag}_bench_C3.json 2> gpurun_out/${tag}_bench_C3.err
+timeout 300 python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${tag}_bench_C2.json 2> gpurun_out/${tag}_bench_C2.err
 exit 0
