@@ -185,7 +185,6 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_NCONS")) c->env_ncons = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::max(0, std::min(2, std::atoi(s)));
   c->env_no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
-  if (const char* s = std::getenv("TTS_S_AHEAD")) c->env_s_ahead = std::atoi(s);
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;

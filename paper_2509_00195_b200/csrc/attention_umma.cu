@@ -12,7 +12,7 @@
 //             adjacent (ledger C5) -- the ordered list of its
 //             DISTINCT pages, each with its member-beam bitmask and valid-token
 //             count.
-// k_tree_umma a4 (+ a5): persistent, 1 CTA per SM.  A tile is (group, kv
+// k_tree_umma a4 (+ a5): persistent, 2 CTAs per SM.  A tile is (group, kv
 //             head, layer): the group's beams x the G query heads of the kv
 //             head, <= 128 rows, against the group's page list.  Whole tiles
 //             round-robin first, then the rest split over all CTAs (stream-K)
@@ -20,9 +20,7 @@
 // Per unit of two pages:
 //   producer warp   TMA (16x128 bf16 K / fp16 V tiles, SWIZZLE_128B) -> smem ring
 //   S warp          S[128 x 32] = Q . K^T     tcgen05.mma kind::f16, S in TMEM
-//   softmax warps   two warpgroups taking alternate units, each with its own
-//                   online-softmax state and O accumulator (merged per piece);
-//                   one thread per row: tcgen05.ld S; mask rows whose beam does not
+//   softmax warps   one thread per row: tcgen05.ld S; mask rows whose beam does not
 //                   reference the page and token slots >= ntok; fp32 online softmax
 //                   with lazy rescale (O rescaled in TMEM only when the running max
 //                   grows by > 2^8); P in fp16 -> tcgen05.st over S
@@ -44,76 +42,31 @@ constexpr int kP = 16;
 constexpr int kD = 128;
 constexpr int kRows = 128;
 constexpr int kU = 2;                        // pages per unit
-constexpr int kNS = 12;                      // TMA ring slots (units)
-constexpr int kNSB = 6;                      // S/P buffers in TMEM (3 per softmax warpgroup)
+constexpr int kNS = 6;                       // ring slots (units)
 constexpr int kTile = kP * kD * 2;           // 4 KiB: one (page, kv head) K or V tile
 constexpr int kSlot = 2 * kU * kTile;        // 16 KiB: K tiles then V tiles
-constexpr int kRing = kNS * kSlot;           // 192 KiB
-constexpr int kSoftWarps = 8;                // two softmax warpgroups
-constexpr int kWarpProducer = 8, kWarpS = 9, kWarpPV = 10;
-constexpr int kThreads = 32 * 11;
-constexpr int kTmemCols = 512;               // O_0 [0,128), O_1 [128,256), Q [256,320), S/P 6 x 32 [320,512)
-constexpr int kColQ = 256;
-constexpr int kColS = 320;
+constexpr int kRing = kNS * kSlot;           // 64 KiB
+constexpr int kThreads = 224;                // warps 0-3 softmax, 4 producer, 5 S issuer, 6 PV issuer
+constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
 constexpr int kSCols = kU * kP;              // 32
-static_assert(kColS + kNSB * kSCols == kTmemCols, "TMEM budget");
 
 constexpr int kMaxGroups = 1024;             // beam groups per call (smem prefix of their unit counts)
 constexpr int kOffRing = 0;
 constexpr int kOffMeta = kOffRing + kRing;
 constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 3 * kNSB + 3;  // full, empty, sfull, pfull, pv, qready, ofree, qtaken
-constexpr int kOffML = (kOffBar + kNumBars * 8 + 16 + 15) / 16 * 16;  // [2 piece parity][2 WG][128] (m, l)
-constexpr int kOffPre = kOffML + 2 * 2 * kRows * 8;
+constexpr int kNumBars = 2 * kNS + 9;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree, qtaken
+constexpr int kOffScr = (kOffBar + kNumBars * 8 + 16 + 15) / 16 * 16;  // int4 scratch: 16-B aligned
+constexpr int kScrItems = 64;                // producer: one batch of 32 units (2 items each)
+constexpr int kOffPre = kOffScr + kScrItems * 16;
 constexpr int kOffInfo = kOffPre + (kMaxGroups + 1) * 4;
 constexpr int kSmemBytes = kOffInfo + 16 + 1024;
-static_assert(kSmemBytes + 1024 <= 228 * 1024, "one CTA per SM");
-static_assert(2 * (kSmemBytes + 1024) > 228 * 1024, "at most one CTA per SM (plan double-buffer argument)");
-static_assert(kOffML % 16 == 0 && kOffMeta % 16 == 0 && kOffBar % 8 == 0, "shared-memory alignment");
-
-#ifdef TTS_HANG
-// watchdog (tools/hang.py): a wait that spins too long records (tag, barrier,
-// parity, unit) per (CTA, warp) in mapped host memory the host polls
-__device__ int* g_watch;
-__device__ __forceinline__ void bar_wait_w(uint32_t b, uint32_t par, int tag, int js) {
-  uint32_t ok = 0;
-  long long n = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(b), "r"(par)
-        : "memory");
-    if (ok) break;
-    if (++n == 2000000 && (threadIdx.x & 31) == 0 && g_watch) {
-      volatile int* w = g_watch + (blockIdx.x * 12 + (threadIdx.x >> 5)) * 4;
-      w[0] = tag;
-      w[1] = (int)b;
-      w[2] = (int)par;
-      w[3] = js;
-      __threadfence_system();
-    }
-  }
-}
-#define BW(b, par, tag, js) bar_wait_w((b), (par), (tag), (js))
-// progress marker of this warp in the watch slot's last two ints (tag 100+, value)
-#define PMARK(tag, v)                                                         \
-  do {                                                                        \
-    if ((threadIdx.x & 31) == 0 && g_watch) {                                 \
-      volatile int* w_ = g_watch + 400 * 12 * 4 + (blockIdx.x * 12 + (threadIdx.x >> 5)) * 2; \
-      w_[0] = (tag);                                                          \
-      w_[1] = (v);                                                            \
-    }                                                                         \
-  } while (0)
-#else
-#define PMARK(tag, v) do {} while (0)
-#define BW(b, par, tag, js) bar_wait((b), (par))
-#endif
+static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert(3 * (kSmemBytes + 1024) > 228 * 1024, "at most two CTAs per SM (plan double-buffer argument)");
+static_assert(kOffScr % 16 == 0 && kOffMeta % 16 == 0 && kOffBar % 8 == 0, "shared-memory alignment");
 
 #ifdef TTS_PROF
 // per CTA (last launch) x warp: accumulated cycles [0..5] + counters (tools/prof.py)
-__device__ long long g_prof[512][12][16];
+__device__ long long g_prof[512][8][16];
 #define PROF_DECL long long pf_[16] = {}; long long pf_t = clock64()
 #define PROF_MARK(k)                   \
   do {                                 \
@@ -134,6 +87,42 @@ __device__ long long g_prof[512][12][16];
 #define PROF_FLUSH(w) do {} while (0)
 #endif
 
+#ifdef TTS_TRACE
+__device__ long long g_trace[1024][8];
+__device__ long long g_trace2[1024][8];
+__device__ long long g_cta[4096][4];  // per CTA of the last launch: globaltimer at start / loop end / exit, units | smid << 32
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TTS_CTA(ev, v)                                                                          \
+  do {                                                                                          \
+    const int id_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);             \
+    if (id_ < 4096) g_cta[id_][(ev)] = (v);                                                    \
+  } while (0)
+#define TTS_TR(j, ev)                                                                   \
+  do {                                                                                  \
+    if (blockIdx.x == 10 && (j) >= 0 && (j) < 1024) \
+      g_trace[(j)][(ev)] = clock64();                                                   \
+  } while (0)
+#define TTS_TR2(j, ev)                                                                  \
+  do {                                                                                  \
+    if (blockIdx.x == 10 && (j) >= 0 && (j) < 1024) \
+      g_trace2[(j)][(ev)] = clock64();                                                  \
+  } while (0)
+#else
+#define TTS_CTA(ev, v) \
+  do {                 \
+  } while (0)
+#define TTS_TR(j, ev) \
+  do {                \
+  } while (0)
+#define TTS_TR2(j, ev) \
+  do {                 \
+  } while (0)
+#endif
+
 struct UParams {
   const int4* items;          // per-group distinct-page lists (k_plan), group slice at (req * maxB + beam0) * maxP
   const int32_t* counts;      // items per group of the call (k_plan)
@@ -145,12 +134,11 @@ struct UParams {
   float* partial;             // [2 * gridDim.x][m 128 | l 128 | O 128 x 128]: split tiles' partial states
   int32_t* tile_cnt;          // [n_tiles] pieces of a split tile done (reset by its merger)
   int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
-  int s_ahead;                // S MMAs issued at most this many units past the oldest incomplete PV (<= kNSB)
   int64_t num_pages;
   float scale_log2;
 };
 constexpr int kPartFloats = 2 * kRows + kRows * kD;
-constexpr int kMaxCtas = 2 * 160;  // partial-state slots (2 per CTA) are sized for this many CTAs
+constexpr int kMaxCtas = 2 * 160;  // partial-state slots are sized for this many CTAs
 
 // The call's descriptors in the kernel parameter block (no H2D copy on the stream)
 constexpr int kInlineGroups = 32;
@@ -185,7 +173,7 @@ struct PlanParams {
   int n_groups, layer_begin, n_call, Hkv, maxB, maxP;
   int64_t num_pages;
 };
-constexpr int kPlanThreads = 128;  // small enough to co-reside with the attention CTA of an SM
+constexpr int kPlanThreads = 128;  // small enough to co-reside with two attention CTAs per SM
 
 __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __grid_constant__ UInline inl) {
   __shared__ int s_len[32];
@@ -336,32 +324,20 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 }
 
 // ---------------------------------------------------------------------------
-// Persistent attention (a4 + a5), ONE CTA per SM, 11 warps.  The call's work
-// is a sequence of units (2 distinct pages of one tile), tiles ordered (layer,
-// kv head, group) with the group fastest.  Whole tiles go round-robin while
-// there are at least 3/4 as many left as CTAs (phase 1); the units of the rest
-// are split over the CTAs (phase 2, stream-K).  A CTA's phase-2 range covers
-// whole tiles and at most two partial ones; a tile split over several CTAs is
-// merged by the CTA that finishes its piece last (global counter), reading the
+// Persistent attention (a4 + a5), 2 CTAs per SM.  The call's work is a
+// sequence of units (2 distinct pages of one tile), tiles ordered (layer, kv
+// head, group) with the group fastest.  Whole tiles go round-robin while there
+// are at least 3/4 as many left as CTAs (phase 1); the units of the rest are
+// split evenly over the CTAs (phase 2, stream-K).  A CTA's phase-2 range covers whole
+// tiles and at most two partial ones; a tile split over several CTAs is merged
+// by the CTA that finishes its piece last (global counter), reading the
 // pieces' partial (m, l, O) in piece order, so the result does not depend on
 // which CTA finishes first.  Every warp derives the same piece sequence from
 // the per-group unit counts (prefix in smem).
-//
-// Why one CTA with two softmax warpgroups (measured, tools/prof.py +
-// tools/mma_bench.cu): an MMA batch -> commit -> mbarrier round trip costs
-// ~400 cycles, so the S -> softmax -> PV -> (S buffer free) loop of a unit is
-// ~2,500 cycles; with two S buffers per CTA (all a 256-column TMEM share
-// allows next to O and Q) two CTAs per SM reached one unit per ~675 cycles.
-// One CTA owns all 512 TMEM columns: two O accumulators, Q, and SIX S buffers;
-// units alternate between two softmax warpgroups (unit js -> WG js & 1), each
-// with its own online-softmax state (m, l) and O accumulator, merged once per
-// piece in the epilogue.  Each WG keeps three units in flight, and the 12-slot
-// TMA ring (192 KiB) prefetches 12 units.
-// kPoly: exponentials on the FMA/ALU pipes (ex2_poly2) instead of MUFU: 1 = every other pair, 2 = all.
-// (<= 160 registers, so that one 128-thread k_plan block of the next call
-// fits beside the CTA: 352 x 160 + 128 x 64 <= 64 Ki registers)
+// kPoly: exponentials on the FMA/ALU pipes (ex2_poly2) instead of MUFU: 1 = every other pair, 2 = all
+// instead of MUFU.
 template <int kPoly>
-__global__ void __maxnreg__(160)
+__global__ void __launch_bounds__(kThreads, 2)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
   extern __shared__ uint8_t smem_raw[];
@@ -371,14 +347,15 @@ __global__ void __maxnreg__(160)
   int4* meta = reinterpret_cast<int4*>(bp + kOffMeta);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bp + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  int* s_pre = reinterpret_cast<int*>(bp + kOffPre);     // [n_groups + 1] exclusive prefix of units per group
-  int* s_info = reinterpret_cast<int*>(bp + kOffInfo);   // [0] merger flag
-  float2* s_ml = reinterpret_cast<float2*>(bp + kOffML);  // [2 parity][2 WG][128 rows] (m, l) of a piece
+  int* s_pre = reinterpret_cast<int*>(bp + kOffPre);  // [n_groups + 1] exclusive prefix of units per group
+  int* s_info = reinterpret_cast<int*>(bp + kOffInfo);  // [0] merger flag
   const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 8 * kNSB, b_pv = b_pfull + 8 * kNSB, b_qready = b_pv + 8 * kNSB,
-                 b_ofree = b_qready + 8, b_qtaken = b_ofree + 8;
+                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_ofree = b_qready + 8,
+                 b_qtaken = b_ofree + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
+  if (threadIdx.x == 0) TTS_CTA(0, gtimer());
   // the next call's k_plan may start as soon as every CTA of this grid runs
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) {
@@ -386,17 +363,17 @@ __global__ void __maxnreg__(160)
       bar_init(b_full + 8 * i, 1);
       bar_init(b_empty + 8 * i, 1);
     }
-    for (int i = 0; i < kNSB; ++i) {
+    for (int i = 0; i < 2; ++i) {
       bar_init(b_sfull + 8 * i, 1);
-      bar_init(b_pfull + 8 * i, 4);  // the 4 warps of the unit's warpgroup
+      bar_init(b_pfull + 8 * i, 4);
       bar_init(b_pv + 8 * i, 1);
     }
-    bar_init(b_qready, kSoftWarps);
-    bar_init(b_ofree, kSoftWarps);
+    bar_init(b_qready, 4);
+    bar_init(b_ofree, 4);
     bar_init(b_qtaken, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kWarpS) {
+  if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -405,9 +382,7 @@ __global__ void __maxnreg__(160)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_q = tmem + kColQ, t_s0 = tmem + kColS;
-  auto t_o = [&](int w) { return tmem + (uint32_t)(w * kD); };
-  auto t_s = [&](int js) { return t_s0 + (uint32_t)((js % kNSB) * kSCols); };
+  const uint32_t t_o = tmem, t_q = tmem + 128, t_s = tmem + 192;
   const int G = p.G;
   const int ng = p.n_groups;
   const int T = p.n_layers * p.Hkv * ng;
@@ -418,14 +393,13 @@ __global__ void __maxnreg__(160)
   if (4 * (T - k1 * Cg) >= 3 * Cg) ++k1;
   const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   auto group_of = [&](int gi) { return p.groups ? p.groups[gi] : inl.g[gi]; };
-  const int quad = warp & 3;              // TMEM lane quadrant of a softmax warp
-  const int wg = warp >> 2;               // softmax warpgroup (warps < 8)
-  const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-  const int r = quad * 32 + lane;         // this thread's tile row (softmax warps)
-  // Rows of a tile, balanced over the four lane quadrants: quadrant q holds
-  // beams [q*bpw, (q+1)*bpw) of the group, G consecutive lanes per beam (host:
-  // bpw * G <= 32).  A page's exponentials are computed only by the warps
-  // holding one of its member beams.
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const int r = threadIdx.x;
+  // Rows of a tile, balanced over the four lane quadrants (softmax warps):
+  // warp w holds beams [w*bpw, (w+1)*bpw) of the group, G consecutive lanes
+  // per beam (host: bpw * G <= 32).  A page's exponentials are computed only
+  // by the warps holding one of its member beams, so spreading the beams
+  // evenly spreads the softmax work of private pages over all four warps.
   auto row_of = [&](const GroupDesc& g, int row, int& beam, int& head) {
     const int bpw = (g.nbeams + 3) >> 2;
     const int l = row & 31, bw = l / G;
@@ -433,8 +407,7 @@ __global__ void __maxnreg__(160)
     head = l - bw * G;
     return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
   };
-  // Q rows of a piece -> TMEM (the A operand of S = Q K^T): lane = row,
-  // column = d pair; warpgroup w loads the d half w
+  // Q rows of a piece -> TMEM (the A operand of S = Q K^T): lane = row, column = d pair
   auto load_q = [&](int gi, int slab) {
     const GroupDesc g = group_of(gi);
     int bl, hd;
@@ -443,16 +416,19 @@ __global__ void __maxnreg__(160)
     const uint4* src = reinterpret_cast<const uint4*>(
         p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (ok ? bl : 0)) * p.Hq + kh * G +
                (ok ? hd : 0)) * kD);
-    uint32_t h[32];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 v = ok ? __ldg(src + wg * 8 + c) : make_uint4(0, 0, 0, 0);
-      h[4 * c] = v.x;
-      h[4 * c + 1] = v.y;
-      h[4 * c + 2] = v.z;
-      h[4 * c + 3] = v.w;
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t h[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = ok ? __ldg(src + hf * 8 + c) : make_uint4(0, 0, 0, 0);
+        h[4 * c] = v.x;
+        h[4 * c + 1] = v.y;
+        h[4 * c + 2] = v.z;
+        h[4 * c + 3] = v.w;
+      }
+      tc_st32(t_q + lane_off + hf * 32, h);
     }
-    tc_st32(t_q + lane_off + wg * 32, h);
     tc_wait_st();
     tc_fence_before();
     __syncwarp();
@@ -460,7 +436,7 @@ __global__ void __maxnreg__(160)
   };
   // the first phase-1 tile (blockIdx.x) is known without the plan: its Q goes
   // to TMEM while k_plan still runs (q is not written by k_plan)
-  if (warp < kSoftWarps && n1 > 0) load_q((int)blockIdx.x % ng, (int)blockIdx.x / ng);
+  if (warp < 4 && n1 > 0) load_q((int)blockIdx.x % ng, (int)blockIdx.x / ng);
   // Programmatic dependent launch: this grid starts while k_plan (the call's
   // append + plan) runs; everything below reads what k_plan writes.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -494,12 +470,12 @@ __global__ void __maxnreg__(160)
   auto F = [&](int t) { return (int64_t)(t / ng) * S + s_pre[t % ng]; };  // first unit of tile t
   const int64_t base2 = F(min(k1 * Cg, T));
   const int64_t U2 = U - base2;
+  // phase-2 CTAs: every one gets >= 1 unit (a split tile's pieces are then
+  // exactly the CTAs whose ranges meet it)
   // Balanced split (when phase 1 ran and every tile is smaller than a CTA's
   // fair share U / C): CTA c's phase-2 range tops its phase-1 tiles up to
   // ~(c+1) U / C units in total, start2(c) = base2 + c U / C - (phase-1 units
-  // of CTAs < c).  Otherwise an even split of the phase-2 units (every
-  // phase-2 CTA gets >= 1 unit, so a split tile's pieces are exactly the CTAs
-  // whose ranges meet it).
+  // of CTAs < c).  Otherwise an even split of the phase-2 units.
   int maxu = 0;
   for (int i = 0; i < ng; ++i) maxu = max(maxu, s_pre[i + 1] - s_pre[i]);
   const bool bal = k1 > 0 && U2 > 0 && (int64_t)k1 * maxu + 1 <= U / Cg;
@@ -554,14 +530,14 @@ __global__ void __maxnreg__(160)
     pslot = 2 * blockIdx.x + (u == ua2 ? 0 : 1);
   };
 
-  if (warp == kWarpProducer) {
+  if (warp == 4) {
     // ========================= producer: TMA =========================
-    // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
-    PROF_DECL;
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
     }
+    // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
+    PROF_DECL;
     int slot = 0;
     uint32_t ph = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
@@ -577,7 +553,7 @@ __global__ void __maxnreg__(160)
       // elected lane writes the slot's metadata and issues the TMAs
       auto issue = [&](const int4& m0, const int4& m1) {
         PROF_MARK(1);
-        BW(b_empty + 8 * slot, ph ^ 1u, 1, slot);
+        bar_wait(b_empty + 8 * slot, ph ^ 1u);
         PROF_MARK(0);
         if (elect_one()) {
           meta[slot * kU] = m0;
@@ -630,61 +606,58 @@ __global__ void __maxnreg__(160)
         PROF_MARK(1);
       }
     }
-    PROF_FLUSH(kWarpProducer);
-  } else if (warp == kWarpS) {
+    PROF_FLUSH(4);
+  } else if (warp == 5) {
     // ========================= S issuer: S = Q K^T =========================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
     // elected lane issues.  S and PV are issued by two warps so that neither
     // waits behind the other's issue (the tensor pipe runs both in issue order).
-    // (TTS_PROF: [0] waiting for K, [1] waiting for the S buffer, [2] issuing, [3] waiting for Q)
     constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
     const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);  // K tiles: K-major SW128
+    // (TTS_PROF: [0] waiting for K, [1] waiting for the S buffer, [2] issuing, [3] waiting for Q)
     PROF_DECL;
     int js = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
       PROF_MARK(2);
-      BW(b_qready, pc & 1, 2, pc);  // this piece's Q in TMEM
+      bar_wait(b_qready, pc & 1);  // this piece's Q in TMEM
       PROF_MARK(3);
       // an empty piece issues no MMA: release its Q explicitly, so that the
       // softmax warps load the next Q only after this wait (no parity aliasing)
       if (j1 == j0 && lane == 0) bar_arrive(b_qtaken);
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNS;
+        if (lane == 0) TTS_TR(js, 0);
         PROF_MARK(2);
-        BW(b_full + 8 * slot, (js / kNS) & 1u, 3, js);
+        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
         PROF_MARK(0);
-        // S buffer js % kNSB holds P(js - kNSB) until PV(js - kNSB) has read it;
-        // run-ahead limited to p.s_ahead units past the oldest PV not yet
-        // complete (the tensor pipe runs in issue order: S MMAs of units far
-        // ahead would delay the PV MMAs the softmax is waiting on)
-        if (js >= p.s_ahead) {
-          const int jw = js - p.s_ahead;
-          BW(b_pv + 8 * (jw % kNSB), (jw / kNSB) & 1u, 4, js);
-        }
+        if (lane == 0) TTS_TR(js, 1);
+        // S buffer js & 1 holds P(js - 2) until PV(js - 2) has read it
+        if (js >= 2) bar_wait(b_pv + 8 * (js & 1), ((js - 2) >> 1) & 1u);
         PROF_MARK(1);
         tc_fence_after();
         // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
         // absent second page leaves columns 16..31 undefined; they are masked)
-        const uint32_t sd = t_s(js);
+        const uint32_t sd = t_s + (js & 1) * kSCols;
         const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
             mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s, ks > 0);
-          tc_commit(b_sfull + 8 * (js % kNSB));
+          tc_commit(b_sfull + 8 * (js & 1));
         }
         __syncwarp();
+        if (lane == 0) TTS_TR(js, 7);
       }
     }
     PROF_MARK(2);
-    PROF_FLUSH(kWarpS);
-  } else if (warp == kWarpPV) {
-    // ====================== PV issuer: O_w += P V ======================
-    // (TTS_PROF: [0] waiting for V, [1] waiting for P, [2] waiting for O, [3] issuing)
+    PROF_FLUSH(5);
+  } else if (warp == 6) {
+    // ====================== PV issuer: O += P V ======================
     constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
     const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
+    // (TTS_PROF: [0] waiting for V, [1] waiting for P, [2] waiting for O, [3] issuing)
     PROF_DECL;
     int js = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
@@ -692,50 +665,48 @@ __global__ void __maxnreg__(160)
       piece(pc, gi, slab, j0, j1, pslot);
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNS;
-        const int w = js & 1;
         PROF_MARK(3);
-        BW(b_full + 8 * slot, (js / kNS) & 1u, 5, js);
+        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
         PROF_MARK(0);
-        BW(b_pfull + 8 * (js % kNSB), (js / kNSB) & 1u, 6, js);
+        bar_wait(b_pfull + 8 * (js & 1), (js >> 1) & 1u);
         PROF_MARK(1);
-        // the first PV of a warpgroup in a piece overwrites its O: the
-        // previous piece's epilogue must have read it
-        const bool first = j - j0 < 2;
-        if (first && pc > 0) BW(b_ofree, (pc - 1) & 1, 7, js);
+        // the first PV of a piece overwrites O: the previous piece's epilogue must have read it
+        if (j == j0 && pc > 0) bar_wait(b_ofree, (pc - 1) & 1);
         PROF_MARK(2);
+        if (lane == 0) TTS_TR(js, 2);
         tc_fence_after();
-        const uint32_t pa = t_s(js);
+        const uint32_t pa = t_s + (js & 1) * kSCols;
         const bool e = elect_one();
-        uint32_t acc = !first;
+        uint32_t acc = j != j0;
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
           if (meta[slot * kU + k].x < 0) continue;
           const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
-          if (e) mma_ts(t_o(w), pa + k * (kP / 2), dv, id_pv, acc);
+          if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
           acc = 1;
         }
         if (e) {
           // S(js) completed before the softmax produced P(js), so this commit
           // covers every read of the slot
           tc_commit(b_empty + 8 * slot);
-          tc_commit(b_pv + 8 * (js % kNSB));
+          tc_commit(b_pv + 8 * (js & 1));
+          TTS_TR(js, 3);
         }
         __syncwarp();
       }
     }
     PROF_MARK(3);
-    PROF_FLUSH(kWarpPV);
-  } else if (warp < kSoftWarps) {
-    // ================= softmax: warpgroup wg takes the units js with js & 1 == wg =================
-    // (TTS_PROF: [0] waiting for S, [1] softmax of member units, [2] skipped units,
-    //  [3] other, [4] rescales, [5] P store + arrive, [6] member units, [7] own units,
-    //  [8] load Q, [9] wait last PV, [10] O store / partial, [11] merge, [12] merges)
-    PROF_DECL;
+    PROF_FLUSH(6);
+  } else if (warp < 4) {
+    // ============================ softmax (warps 0-3) ============================
     if (n_pieces > 0 && n1 == 0) {  // first piece in phase 2: Q after the plan
       int gi, slab, j0, j1, pslot;
       piece(0, gi, slab, j0, j1, pslot);
       load_q(gi, slab);
     }
+    // (TTS_PROF: [0] waiting for S, [1] softmax of member units, [2] skipped units,
+    //  [3] epilogue + Q loads, [4] rescales, [5] P store + arrive; [6] member units, [7] all units)
+    PROF_DECL;
     int js = 0, n_empty = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
@@ -745,14 +716,13 @@ __global__ void __maxnreg__(160)
       const bool rvalid = row_of(g, r, rbl, rh);
       const int lrel = slab / p.Hkv, kh = slab % p.Hkv;
       float m_ref = -1e30f, l = 0.f;
-      bool own_seen = false;
       for (int j = j0; j < j1; ++j, ++js) {
-        if ((js & 1) != wg) continue;
-        PMARK(101, js);
+        if (r == 0) TTS_TR(js, 4);
         PROF_MARK(3);
-        BW(b_sfull + 8 * (js % kNSB), (js / kNSB) & 1u, 8, js);
+        bar_wait(b_sfull + 8 * (js & 1), (js >> 1) & 1u);
         PROF_MARK(0);
         PROF_CNT(7);
+        if (r == 0) TTS_TR(js, 5);
         tc_fence_after();
         const int slot = js % kNS;
         int4 mt[kU];
@@ -770,7 +740,6 @@ __global__ void __maxnreg__(160)
         uint32_t pk[kSCols / 2];
 #pragma unroll
         for (int i = 0; i < kSCols / 2; ++i) pk[i] = 0u;
-        const uint32_t ts = t_s(js) + lane_off;
         if (wany) {
           float v[kSCols];
           {
@@ -778,13 +747,13 @@ __global__ void __maxnreg__(160)
             // shared per-SM resource (a private page is read by one warp)
             uint32_t sr[kSCols];
             if (wm[0] && wm[1]) {
-              tc_ld32(ts, sr);
+              tc_ld32(t_s + lane_off + (js & 1) * kSCols, sr);
               tc_wait_ld();
 #pragma unroll
               for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
             } else {
               const int pg = wm[0] ? 0 : 1;
-              tc_ld16(ts + pg * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
+              tc_ld16(t_s + lane_off + (js & 1) * kSCols + pg * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
               tc_wait_ld();
 #pragma unroll
               for (int i = 0; i < kP; ++i) {
@@ -813,21 +782,21 @@ __global__ void __maxnreg__(160)
           }
           mx *= p.scale_log2;
           const bool need = mx > m_ref + 8.0f;
-          if (__any_sync(0xffffffffu, need) && own_seen) {
+          if (__any_sync(0xffffffffu, need) && j > j0) {
+            if (r == 0) TTS_TR2(js, 7);
             PROF_MARK(1);
-            // every earlier PV into this warpgroup's O (the last was unit js - 2)
-            // must have landed before O is rescaled in TMEM
-            BW(b_pv + 8 * ((js - 2) % kNSB), ((js - 2) / kNSB) & 1u, 9, js);
+            // every earlier PV product must have landed before O is rescaled in TMEM
+            bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
             tc_fence_after();
             const float alpha = need ? exp2f(m_ref - mx) : 1.f;
 #pragma unroll 1
             for (int ch = 0; ch < 4; ++ch) {
               uint32_t o[32];
-              tc_ld32(t_o(wg) + lane_off + ch * 32, o);
+              tc_ld32(t_o + lane_off + ch * 32, o);
               tc_wait_ld();
 #pragma unroll
               for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tc_st32(t_o(wg) + lane_off + ch * 32, o);
+              tc_st32(t_o + lane_off + ch * 32, o);
             }
             tc_wait_st();
             l *= alpha;
@@ -864,26 +833,20 @@ __global__ void __maxnreg__(160)
         } else {
           PROF_MARK(2);
         }
-        own_seen = true;
         // P (fp16) over the unit's first 16 S columns (value c at column c/2)
-        tc_st16(ts, pk);
+        tc_st16(t_s + lane_off + (js & 1) * kSCols, pk);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) bar_arrive(b_pfull + 8 * (js % kNSB));
-        PMARK(102, js);
+        if (r == 0) TTS_TR(js, 6);
+        if (lane == 0) TTS_TR2(js, warp);
+        if (lane == 0) bar_arrive(b_pfull + 8 * (js & 1));
         PROF_MARK(5);
       }
-      const int n_units = j1 - j0;
-      // the next piece's Q, once every S MMA of this piece has completed (the
-      // last unit's S, of either warpgroup: S MMAs complete in issue order)
+      // the next piece's Q (every S MMA of this piece has completed), so that
+      // its S = Q K^T overlaps this piece's epilogue
       if (pc + 1 < n_pieces) {
-        if (n_units == 0) {
-          BW(b_qtaken, (n_empty++) & 1, 10, js);
-        } else {
-          const int jl = js - 1;
-          BW(b_sfull + 8 * (jl % kNSB), (jl / kNSB) & 1u, 11, jl);
-        }
+        if (j1 == j0) bar_wait(b_qtaken, (n_empty++) & 1);  // (a non-empty piece: its S MMAs read Q)
         int gi2, slab2, j02, j12, ps2;
         piece(pc + 1, gi2, slab2, j02, j12, ps2);
         PROF_MARK(3);
@@ -894,189 +857,157 @@ __global__ void __maxnreg__(160)
       // (an empty piece -- a tile with no units, e.g. under a sticky error --
       // writes nothing)
       const int tu = s_pre[gi + 1] - s_pre[gi];
-      if (n_units > 0) {
-        // every PV of the piece has landed (PVs complete in issue order)
-        const int jl = js - 1;
-        BW(b_pv + 8 * (jl % kNSB), (jl / kNSB) & 1u, 12, jl);
-        PROF_MARK(9);
-        tc_fence_after();
-        // the two warpgroups' (m, l) of every row, then warpgroup w combines
-        // output columns [64 w, 64 w + 64) of O_0 and O_1
-        const bool mine = own_seen;
-        // (double-buffered by piece parity: the other warpgroup may still read
-        // the previous piece's pair when this one is written)
-        float2* ml = s_ml + (pc & 1) * 2 * kRows;
-        ml[wg * kRows + r] = make_float2(mine ? m_ref : -INFINITY, mine ? l : 0.f);
-        PMARK(103, pc);
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        PMARK(104, pc);
-        const float2 ml0 = ml[r], ml1 = ml[kRows + r];
-        const float M = fmaxf(ml0.x, ml1.x);
-        const float a0 = ml0.y > 0.f ? exp2f(ml0.x - M) : 0.f;
-        const float a1 = ml1.y > 0.f ? exp2f(ml1.x - M) : 0.f;
-        const float L = ml0.y * a0 + ml1.y * a1;
-        // O chunk ch (32 columns) of the combined, unnormalised accumulator
-        // (tcgen05.ld is warp-collective: the loads are warp-uniform, the weights
-        // per row; an accumulator a row's warpgroup never wrote is selected
-        // away, never multiplied -- it may hold anything)
-        const bool u0 = __any_sync(0xffffffffu, a0 > 0.f), u1 = __any_sync(0xffffffffu, a1 > 0.f);
-        auto o_chunk = [&](int ch, float (&o)[32]) {
-          uint32_t x[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = 0.f;
-          if (u0) {
-            tc_ld32(t_o(0) + lane_off + ch * 32, x);
-            tc_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = a0 > 0.f ? __uint_as_float(x[i]) * a0 : 0.f;
-          }
-          if (u1) {
-            tc_ld32(t_o(1) + lane_off + ch * 32, x);
-            tc_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] += a1 > 0.f ? __uint_as_float(x[i]) * a1 : 0.f;
-          }
-        };
-        float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD;
-        PMARK(110, tu);
-        if (j0 == 0 && j1 == tu) {
-          const float inv = 1.f / L;
+      if (j1 > j0) {
+      bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
+      PROF_MARK(9);
+      tc_fence_after();
+      float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD;
+      if (j0 == 0 && j1 == tu) {
+        const float inv = 1.f / l;
 #pragma unroll 1
-          for (int ch = 2 * wg; ch < 2 * wg + 2; ++ch) {
-            float o[32];
-            o_chunk(ch, o);
-            if (rvalid) {
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t o[32];
+          tc_ld32(t_o + lane_off + ch * 32, o);
+          tc_wait_ld();
+          if (rvalid) {
 #pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *reinterpret_cast<float4*>(orow + ch * 32 + i) =
-                    make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
-            }
-          }
-          PROF_MARK(10);
-        } else {
-          // a5: this piece's (M, L, unnormalised O) -> its partial slot (2c for the
-          // CTA's first phase-2 piece, 2c + 1 for its last); O stored chunk-major
-          // ([32 chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
-          // The last piece to finish merges.
-          float* part = p.partial + (size_t)pslot * kPartFloats;
-          PMARK(111, pslot);
-          if (wg == 0) {
-            part[r] = M;
-            part[kRows + r] = L;
-          }
-          float4* po = reinterpret_cast<float4*>(part + 2 * kRows) + r;
-#pragma unroll 1
-          for (int ch = 2 * wg; ch < 2 * wg + 2; ++ch) {
-            float o[32];
-            o_chunk(ch, o);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              __stcg(po + (ch * 8 + i) * kRows, make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
-          }
-          PMARK(112, 0);
-          __threadfence();
-          PMARK(113, 0);
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          PMARK(114, 0);
-          const int64_t T0 = F(slab * ng + gi);
-          auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
-            if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
-            int lo = 0, hi = C2;  // largest c with start2(c) <= x
-            while (hi - lo > 1) {
-              const int mid = (lo + hi) >> 1;
-              if (start2(mid) <= x) lo = mid;
-              else hi = mid;
-            }
-            return lo;
-          };
-          const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
-          const int tile = slab * ng + gi;
-          PMARK(105, pc);
-          if (threadIdx.x == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          PMARK(106, pc);
-          PROF_MARK(10);
-          if (s_info[0]) {
-            __threadfence();
-            const int np = c_last - c_first + 1;
-            // piece k's slot: only the first CTA's range can start before the tile
-            const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
-            auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
-            // latency-bound (L2 round trips under full HBM load): every batch of
-            // loads is issued before any is consumed
-            float Mm = -INFINITY, Lm = 0.f;
-            for (int k0 = 0; k0 < np; k0 += 8) {
-              float mv[8], lv[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const bool ok = k0 + i < np;
-                mv[i] = ok ? __ldcg(part_of(k0 + i) + r) : -INFINITY;
-                lv[i] = ok ? __ldcg(part_of(k0 + i) + kRows + r) : 0.f;
-              }
-              float M2 = Mm;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) M2 = fmaxf(M2, mv[i]);
-              Lm *= exp2f(Mm - M2);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) Lm += k0 + i < np ? exp2f(mv[i] - M2) * lv[i] : 0.f;
-              Mm = M2;
-            }
-            const float inv = 1.f / Lm;
-#pragma unroll 1
-            for (int ch = 2 * wg; ch < 2 * wg + 2; ++ch) {
-              float4 acc4[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int k = 0; k < np; k += 2) {
-                const bool two = k + 1 < np;
-                const float* pa = part_of(k);
-                const float* pb = part_of(two ? k + 1 : k);
-                const float wa = __ldcg(pa + r), wb = __ldcg(pb + r);
-                const float4* sa = reinterpret_cast<const float4*>(pa + 2 * kRows) + r;
-                const float4* sb = reinterpret_cast<const float4*>(pb + 2 * kRows) + r;
-                float4 xa[8], xb[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  xa[i] = __ldcg(sa + (ch * 8 + i) * kRows);
-                  xb[i] = __ldcg(sb + (ch * 8 + i) * kRows);
-                }
-                const float fa = exp2f(wa - Mm), fb = two ? exp2f(wb - Mm) : 0.f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  acc4[i].x += fa * xa[i].x + fb * xb[i].x;
-                  acc4[i].y += fa * xa[i].y + fb * xb[i].y;
-                  acc4[i].z += fa * xa[i].z + fb * xb[i].z;
-                  acc4[i].w += fa * xa[i].w + fb * xb[i].w;
-                }
-              }
-              if (rvalid) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  *reinterpret_cast<float4*>(orow + ch * 32 + 4 * i) =
-                      make_float4(acc4[i].x * inv, acc4[i].y * inv, acc4[i].z * inv, acc4[i].w * inv);
-              }
-            }
-            // every piece of the tile has arrived: ready for the next call
-            // (both warpgroups have read the slots' m/l before thread 0 resets)
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            if (threadIdx.x == 0) p.tile_cnt[tile] = 0;
-            PROF_MARK(11);
-            PROF_CNT(12);
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(orow + ch * 32 + i) =
+                  make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                              __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
           }
         }
+      } else {
+        // a5: this piece's (m, l, unnormalised O) -> its partial slot (2c for the
+        // CTA's first phase-2 piece, 2c + 1 for its last); O stored chunk-major
+        // ([32 chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
+        // The last piece to finish merges.
+        float* part = p.partial + (size_t)pslot * kPartFloats;
+        part[r] = m_ref;
+        part[kRows + r] = l;
+        float4* po = reinterpret_cast<float4*>(part + 2 * kRows) + r;
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t o[32];
+          tc_ld32(t_o + lane_off + ch * 32, o);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            __stcg(po + (ch * 8 + i) * kRows,
+                   make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
+                               __uint_as_float(o[4 * i + 3])));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int64_t T0 = F(slab * ng + gi);
+        auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
+          if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
+          int lo = 0, hi = C2;  // largest c with start2(c) <= x
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (start2(mid) <= x) lo = mid;
+            else hi = mid;
+          }
+          return lo;
+        };
+        const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
+        const int tile = slab * ng + gi;
+        if (r == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        PROF_MARK(10);
+        if (s_info[0]) {
+          __threadfence();
+          const int np = c_last - c_first + 1;
+          // piece k's slot: only the first CTA's range can start before the tile
+          const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
+          auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
+          // latency-bound (L2 round trips under full HBM load): every batch of
+          // loads is issued before any is consumed
+          float M = -INFINITY, L = 0.f;
+          for (int k0 = 0; k0 < np; k0 += 8) {
+            float mv[8], lv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const bool ok = k0 + i < np;
+              mv[i] = ok ? __ldcg(part_of(k0 + i) + r) : -INFINITY;
+              lv[i] = ok ? __ldcg(part_of(k0 + i) + kRows + r) : 0.f;
+            }
+            float M2 = M;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) M2 = fmaxf(M2, mv[i]);
+            L *= exp2f(M - M2);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) L += k0 + i < np ? exp2f(mv[i] - M2) * lv[i] : 0.f;
+            M = M2;
+          }
+          const float inv = 1.f / L;
+#pragma unroll 1
+          for (int ch = 0; ch < 4; ++ch) {
+            float4 acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < np; k += 2) {
+              const bool two = k + 1 < np;
+              const float* pa = part_of(k);
+              const float* pb = part_of(two ? k + 1 : k);
+              const float wa = __ldcg(pa + r), wb = __ldcg(pb + r);
+              const float4* sa = reinterpret_cast<const float4*>(pa + 2 * kRows) + r;
+              const float4* sb = reinterpret_cast<const float4*>(pb + 2 * kRows) + r;
+              float4 xa[8], xb[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                xa[i] = __ldcg(sa + (ch * 8 + i) * kRows);
+                xb[i] = __ldcg(sb + (ch * 8 + i) * kRows);
+              }
+              const float fa = exp2f(wa - M), fb = two ? exp2f(wb - M) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                acc[i].x += fa * xa[i].x + fb * xb[i].x;
+                acc[i].y += fa * xa[i].y + fb * xb[i].y;
+                acc[i].z += fa * xa[i].z + fb * xb[i].z;
+                acc[i].w += fa * xa[i].w + fb * xb[i].w;
+              }
+            }
+            if (rvalid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                *reinterpret_cast<float4*>(orow + ch * 32 + 4 * i) =
+                    make_float4(acc[i].x * inv, acc[i].y * inv, acc[i].z * inv, acc[i].w * inv);
+            }
+          }
+          if (r == 0) p.tile_cnt[tile] = 0;  // every piece of the tile has arrived: ready for the next call
+          PROF_MARK(11);
+          PROF_CNT(12);
+        }
+      }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) bar_arrive(b_ofree);  // the next piece's first PVs may overwrite O_0 / O_1
-      PMARK(107, pc);
+      if (lane == 0) bar_arrive(b_ofree);  // the next piece's first PV may overwrite O
     }
     PROF_MARK(3);
     PROF_FLUSH(warp);
   }
 
+  if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
+  if (threadIdx.x == 0) TTS_CTA(1, gtimer());
   tc_fence_before();
   __syncthreads();
-  if (warp == kWarpS) {
+  if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
+  if (threadIdx.x == 0) TTS_CTA(2, gtimer());
+#ifdef TTS_TRACE
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    long long units = ub2 - ua2;
+    for (int k = 0; k < n1; ++k) {
+      const int t = blockIdx.x + k * Cg, gi = t % ng;
+      units += s_pre[gi + 1] - s_pre[gi];
+    }
+    TTS_CTA(3, units | ((long long)smid << 32));
+  }
+#endif
+  if (warp == 5) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
@@ -1084,26 +1015,19 @@ __global__ void __maxnreg__(160)
 
 }  // namespace
 
-#ifdef TTS_HANG
-// mapped host watch buffer of n ints (host pointer returned; the kernel writes it)
-extern "C" int tts_debug_watch_alloc(int n, void** host_h) {
-  int* h = nullptr;
-  if (cudaHostAlloc((void**)&h, (size_t)n * 4, cudaHostAllocMapped) != cudaSuccess) return 1;
-  memset(h, 0, (size_t)n * 4);
-  int* d = nullptr;
-  if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) return 2;
-  if (cudaMemcpyToSymbol(tts::g_watch, &d, sizeof(d)) != cudaSuccess) return 3;
-  *host_h = h;
-  return 0;
-}
-#endif
-
 #ifdef TTS_PROF
 extern "C" int tts_debug_read_prof(long long* out_h) {
   return (int)cudaMemcpyFromSymbol(out_h, g_prof, sizeof(g_prof));
 }
 #endif
 
+#ifdef TTS_TRACE
+extern "C" int tts_debug_read_trace(long long* out_h) {
+  int e = (int)cudaMemcpyFromSymbol(out_h, g_trace, sizeof(g_trace));
+  e = e ? e : (int)cudaMemcpyFromSymbol(out_h + 1024 * 8, g_trace2, sizeof(g_trace2));
+  return e ? e : (int)cudaMemcpyFromSymbol(out_h + 2 * 1024 * 8, g_cta, sizeof(g_cta));
+}
+#endif
 
 size_t umma_partial_bytes() { return (size_t)2 * kMaxCtas * kPartFloats * 4; }
 int umma_max_groups() { return kMaxGroups; }
@@ -1115,12 +1039,12 @@ bool umma_supported(const Ctx* c) {
 }
 
 // Per device context: the kernel attributes, and the residency argument the
-// plan's double buffer relies on.  The grid is exactly one CTA per SM and at
-// most one fits per SM (static_assert on the shared memory above), so all
-// CTAs of call N+1 being resident implies call N's attention kernel has
-// exited -- and call N+2's k_plan (PDL-released by call N+1's CTAs) can only
-// then overwrite the plan buffer call N read.  A device with more SMs than
-// the partial-state slots cover uses the mma.sync path.
+// plan's double buffer relies on.  The grid is exactly two CTAs per SM and at
+// most two fit per SM (static_assert on the shared memory below), so all CTAs
+// of call N+1 being resident implies call N's attention kernel has exited --
+// and call N+2's k_plan (PDL-released by call N+1's CTAs) can only then
+// overwrite the plan buffer call N read.  A device with more SMs than the
+// partial-state slots cover uses the mma.sync path.
 cudaError_t umma_prepare(Ctx* c) {
   c->umma_ok = false;
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
@@ -1128,13 +1052,14 @@ cudaError_t umma_prepare(Ctx* c) {
   for (auto k : {k_tree_umma<0>, k_tree_umma<1>, k_tree_umma<2>}) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
+    // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, kSmemBytes);
     if (e != cudaSuccess) return e;
     c->umma_occupancy = occ;  // diagnostics only (the occupancy API under-reports with the carveout hint)
-    if (c->num_sms > kMaxCtas / 2) return cudaSuccess;
+    if (2 * c->num_sms > kMaxCtas) return cudaSuccess;
   }
   c->umma_ok = true;
   return cudaSuccess;
@@ -1192,7 +1117,6 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.tile_cnt = c->ws_tile_cnt;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
-  p.s_ahead = c->env_s_ahead > 0 ? std::min(c->env_s_ahead, kNSB) : kNSB;
   UInline inl;  // host staging of the parameter block (copied by the launch)
   if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {
     std::memcpy(inl.g, groups_h, (size_t)n_groups * sizeof(GroupDesc));
@@ -1226,7 +1150,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c->num_sms);  // persistent: one CTA per SM (<= kMaxCtas, umma_prepare)
+  // persistent: two CTAs per SM (the smem / TMEM / register budget of one CTA)
+  cfg.gridDim = dim3(2 * c->num_sms);  // persistent: two CTAs per SM (<= kMaxCtas, umma_prepare)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;

@@ -107,7 +107,6 @@ struct Ctx {
   int env_poly = 0;           // TTS_POLY=1: polynomial exp2 for every other pair, 2: for all
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
-  int env_s_ahead = 0;        // TTS_S_AHEAD: S run-ahead of the tcgen05 kernel (units, <= 6)
   int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
   // multi-GPU (span.cu)
   Comm* comm = nullptr;
