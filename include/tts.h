@@ -224,6 +224,53 @@ tts_status_t tts_beam_select_fork_policy(tts_ctx_t ctx, int32_t n_req, const int
                                          const float* scores, int32_t policy, int32_t param,
                                          int32_t* parent_out, void* stream);
 
+/* ---- f1: Speculative Beam Extension, decode side (PAPER.md 4.1, Alg. 1
+ * P:324-350; DESIGN.md ledger C25-C29) ------------
+ * While the stragglers of a step still generate, the slots of finished beams
+ * run speculative branches of finished beams (SelectSpec); verification and
+ * selection see only the non-speculative step (algorithmic equivalence); the
+ * fork then continues children from the branches (DuplicateThenTruncate).
+ * The serving loop calls, per iteration: tts_spec_select (which finished
+ * beams get how many new branches), tts_spec_branch (the rows), the decode
+ * step over originals still in their step + branches; at the step end:
+ * tts_beam_select_global over the N original scores (parent map), tts_spec_plan
+ * (children's source rows and lengths), tts_beam_fork_map_trunc. */
+
+/* SelectSpec (host only, no context): candidate i (beam beam_h[i], previous
+ * score last_score_h[i], have_h[i] branches already) has potential M_i =
+ * B - j + 1, j = ceil((1 - s) B) clamped to [1, B] (s clamped to [0, 1], NaN ->
+ * 0; fp64); candidates in (M desc, beam asc) order get min(M_i - have_i, free)
+ * new branches until free_slots run out.  add_h[i] receives the count. */
+tts_status_t tts_spec_select(int32_t n, const int32_t* beam_h, const float* last_score_h, const int32_t* have_h,
+                             int32_t free_slots, int32_t B, int32_t* add_h);
+
+/* Appends n rows to request req, row n_rows + i a fork of row src_rows_h[i]
+ * (table and length copied, one more reference per page, a partially filled
+ * last page copied into the lowest free page -- ledger C6/C7).  The new rows
+ * take part in later decode calls (the request's beam count grows by n). */
+tts_status_t tts_spec_branch(tts_ctx_t ctx, int32_t req, int32_t n, const int32_t* src_rows_h, void* stream);
+
+/* DuplicateThenTruncate plan (host only): parent_h [N] the selection's parent
+ * map (child -> surviving beam < N); branches: spare row N + i forked from
+ * beam branch_src_h[i] with branch_tokens_h[i] speculative tokens; lens_h [N]
+ * the beams' lengths; frac_h [N] the truncation fraction f of child c (used
+ * when c is not the first child of its survivor); next_len_h [N] (nullable)
+ * caps the kept tokens at the child's next step length.  Child c = r M + j of
+ * survivor s continues branch j of s (the j-th created) when s has one, with
+ * h = n (j = 0) or floor(f n) (j >= 1) of its tokens, else duplicates s
+ * (h = 0).  Outputs parent_rows_h [N], new_len_h [N] (= lens[s] + h), head_h [N]. */
+tts_status_t tts_spec_plan(int32_t N, int32_t M, const int32_t* parent_h, int32_t n_branch,
+                           const int32_t* branch_src_h, const int32_t* branch_tokens_h, const int32_t* lens_h,
+                           const double* frac_h, const int32_t* next_len_h, int32_t* parent_rows_h,
+                           int32_t* new_len_h, int32_t* head_h);
+
+/* tts_beam_fork_map with truncation: new row c keeps the first new_len_h[c]
+ * (1 <= new_len <= the parent row's length) tokens of row parent_h[c]; a kept
+ * partial last page (first child of its parent) has its slots past the new
+ * length cleared, later children copy it (C6).  Syncs. */
+tts_status_t tts_beam_fork_map_trunc(tts_ctx_t ctx, int32_t req, int32_t n_new, const int32_t* parent_h,
+                                     const int32_t* new_len_h, void* stream);
+
 /* ---- a8: one request's beams spanning G GPUs --------------
  * The request's N_global beams are held in G contiguous ranges of global ids
  * (gid = rank * N_local + local index; DFS order across ranks).  Per step:

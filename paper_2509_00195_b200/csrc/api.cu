@@ -2,6 +2,7 @@
 // mirror of beam lengths, launch planning, workspace carving.  Every step of
 // the hot path runs in the kernels of block_table.cu / attention.cu.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -185,6 +186,8 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_NCONS")) c->env_ncons = std::max(0, std::atoi(s));
   if (const char* s = std::getenv("TTS_POLY")) c->env_poly = std::max(0, std::min(2, std::atoi(s)));
   c->env_no_pdl = std::getenv("TTS_NO_PDL") != nullptr;
+  if (const char* s = std::getenv("TTS_ROUND_ROBIN")) c->env_round_robin = std::atoi(s) != 0;
+  if (const char* s = std::getenv("TTS_SPLIT_PARTIAL")) c->env_split_partial = std::atoi(s) != 0;
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
@@ -654,34 +657,167 @@ static void cow_items_for(tts_ctx_t c, int req, int n_new, const int32_t* parent
   }
 }
 
-tts_status_t tts_beam_fork_map(tts_ctx_t c, int32_t req, int32_t n_new, const int32_t* parent_h, void* stream) {
+static tts_status_t fork_map_impl(tts_ctx_t c, int32_t req, int32_t n_new, const int32_t* parent_h,
+                                  const int32_t* new_len_h, void* stream) {
   if (!c || !parent_h || n_new <= 0) return TTS_ERR_INVALID_ARG;
   if (!installed(c, req)) return TTS_ERR_STATE;
   const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
   const int n_old = c->n_rows[req];
   if (n_new > g.max_beams) return TTS_ERR_CAPACITY;
-  for (int i = 0; i < n_new; ++i)
-    if (parent_h[i] < 0 || parent_h[i] >= n_old || c->lens[(int64_t)req * g.max_beams + parent_h[i]] <= 0)
-      return TTS_ERR_INVALID_ARG;
+  const int32_t* lens_old = c->lens.data() + (int64_t)req * g.max_beams;
+  for (int i = 0; i < n_new; ++i) {
+    if (parent_h[i] < 0 || parent_h[i] >= n_old || lens_old[parent_h[i]] <= 0) return TTS_ERR_INVALID_ARG;
+    if (new_len_h && (new_len_h[i] < 1 || new_len_h[i] > lens_old[parent_h[i]])) return TTS_ERR_INVALID_ARG;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   int32_t reqv = req;
   void* dreq = tts::upload(c, &reqv, 4, st, &e);
   TTS_CUDA(e);
+  void* dlen = nullptr;
+  if (new_len_h) {
+    dlen = tts::upload(c, new_len_h, (size_t)n_new * 4, st, &e);
+    TTS_CUDA(e);
+  }
   TTS_CUDA(cudaMemcpyAsync(c->ws_parent, parent_h, (size_t)n_new * 4, cudaMemcpyHostToDevice, st));
-  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, 1, n_old, n_new, st));
+  TTS_CUDA(tts::launch_fork_tables(c, (const int32_t*)dreq, 1, n_old, n_new, st, (const int32_t*)dlen));
   int32_t* lens = c->lens.data() + (int64_t)req * g.max_beams;
   std::vector<int32_t> old(lens, lens + g.max_beams);
-  for (int cc = 0; cc < g.max_beams; ++cc) lens[cc] = cc < n_new ? old[parent_h[cc]] : 0;
+  for (int cc = 0; cc < g.max_beams; ++cc) lens[cc] = cc < n_new ? (new_len_h ? new_len_h[cc] : old[parent_h[cc]]) : 0;
   std::vector<tts::AllocItem> items;
   cow_items_for(c, req, n_new, parent_h, items);
   if (!items.empty()) {
     TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
     TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
   }
+  // a truncated row's kept (first-child) partial last page: clear its slots
+  // past the new length (every token slot of a page past a row's length is 0)
+  if (new_len_h) {
+    std::vector<int32_t> zt;
+    std::vector<char> seen((size_t)g.max_beams, 0);
+    for (int cc = 0; cc < n_new; ++cc) {
+      const int par = parent_h[cc], len = new_len_h[cc];
+      if (!seen[par] && len < old[par] && len % P) zt.insert(zt.end(), {req, cc, (len - 1) / P, len % P});
+      seen[par] = 1;
+    }
+    if (!zt.empty()) {
+      void* dz = tts::upload(c, zt.data(), zt.size() * 4, st, &e);
+      TTS_CUDA(e);
+      TTS_CUDA(tts::launch_zero_tail(c, (const int32_t*)dz, (int)zt.size() / 4, st));
+    }
+  }
   c->n_beams[req] = n_new;
   c->n_rows[req] = n_new;
   TTS_CUDA(cudaStreamSynchronize(st));  // parent_h is a borrowed host buffer
+  return TTS_OK;
+}
+
+tts_status_t tts_beam_fork_map(tts_ctx_t c, int32_t req, int32_t n_new, const int32_t* parent_h, void* stream) {
+  return fork_map_impl(c, req, n_new, parent_h, nullptr, stream);
+}
+
+tts_status_t tts_beam_fork_map_trunc(tts_ctx_t c, int32_t req, int32_t n_new, const int32_t* parent_h,
+                                     const int32_t* new_len_h, void* stream) {
+  if (!new_len_h) return TTS_ERR_INVALID_ARG;
+  return fork_map_impl(c, req, n_new, parent_h, new_len_h, stream);
+}
+
+tts_status_t tts_spec_branch(tts_ctx_t c, int32_t req, int32_t n, const int32_t* src_rows_h, void* stream) {
+  if (!c || n <= 0 || !src_rows_h) return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
+  const int n_old = c->n_rows[req];
+  if (n_old + n > g.max_beams) return TTS_ERR_CAPACITY;
+  int32_t* lens = c->lens.data() + (int64_t)req * g.max_beams;
+  for (int i = 0; i < n; ++i)
+    if (src_rows_h[i] < 0 || src_rows_h[i] >= n_old || lens[src_rows_h[i]] <= 0) return TTS_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  std::vector<int32_t> blob(2 * (size_t)n);
+  std::vector<tts::AllocItem> items;
+  for (int i = 0; i < n; ++i) {
+    const int src = src_rows_h[i], dst = n_old + i, len = lens[src];
+    blob[i] = src;
+    blob[n + i] = dst;
+    if (len % P) items.push_back({entry_of(g, req, dst, (len - 1) / P), 1, len % P});
+  }
+  int32_t* d = (int32_t*)tts::upload(c, blob.data(), blob.size() * 4, st, &e);
+  TTS_CUDA(e);
+  TTS_CUDA(tts::launch_branch_rows(c, req, d, d + n, n, st));
+  if (!items.empty()) {
+    TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
+    TTS_CUDA(tts::launch_cow_copy(c, (int)items.size(), st));
+  }
+  for (int i = 0; i < n; ++i) lens[n_old + i] = lens[src_rows_h[i]];
+  c->n_rows[req] = n_old + n;
+  c->n_beams[req] = n_old + n;
+  return TTS_OK;
+}
+
+tts_status_t tts_spec_select(int32_t n, const int32_t* beam_h, const float* last_score_h, const int32_t* have_h,
+                             int32_t free_slots, int32_t B, int32_t* add_h) {
+  if (n < 0 || B <= 0 || (n > 0 && (!beam_h || !last_score_h || !have_h || !add_h))) return TTS_ERR_INVALID_ARG;
+  std::vector<int> order(n), pot(n);
+  for (int i = 0; i < n; ++i) {
+    // bin j of the previous score over B equal-width bins of [0, 1], the
+    // highest first, a boundary score in the higher bin; potential M = B - j + 1
+    double s = (double)last_score_h[i];
+    if (std::isnan(s)) s = 0.0;
+    s = std::min(1.0, std::max(0.0, s));
+    int j = (int)std::ceil((1.0 - s) * (double)B);
+    j = std::min(B, std::max(1, j));
+    pot[i] = B - j + 1;
+    order[i] = i;
+    add_h[i] = 0;
+  }
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return pot[a] != pot[b] ? pot[a] > pot[b] : beam_h[a] < beam_h[b];
+  });
+  int free = free_slots;
+  for (int i : order) {
+    if (free <= 0) break;
+    const int k = std::min(pot[i] - have_h[i], free);
+    if (k > 0) {
+      add_h[i] = k;
+      free -= k;
+    }
+  }
+  return TTS_OK;
+}
+
+tts_status_t tts_spec_plan(int32_t N, int32_t M, const int32_t* parent_h, int32_t n_branch,
+                           const int32_t* branch_src_h, const int32_t* branch_tokens_h, const int32_t* lens_h,
+                           const double* frac_h, const int32_t* next_len_h, int32_t* parent_rows_h,
+                           int32_t* new_len_h, int32_t* head_h) {
+  if (N <= 0 || M <= 0 || N % M || !parent_h || !lens_h || !frac_h || !parent_rows_h || !new_len_h || !head_h)
+    return TTS_ERR_INVALID_ARG;
+  if (n_branch < 0 || (n_branch > 0 && (!branch_src_h || !branch_tokens_h))) return TTS_ERR_INVALID_ARG;
+  std::vector<std::vector<int>> rows_of(N);
+  for (int i = 0; i < n_branch; ++i) {
+    if (branch_src_h[i] < 0 || branch_src_h[i] >= N) return TTS_ERR_INVALID_ARG;
+    rows_of[branch_src_h[i]].push_back(N + i);
+  }
+  for (int c = 0; c < N; ++c) {
+    const int s = parent_h[c], j = c % M;
+    if (s < 0 || s >= N) return TTS_ERR_INVALID_ARG;
+    if (j < (int)rows_of[s].size()) {
+      // DuplicateThenTruncate: the first child continues the branch intact,
+      // the others keep floor(f n) of its n tokens (f drawn by the caller)
+      const int row = rows_of[s][j];
+      const int n = branch_tokens_h[row - N];
+      int h = j == 0 ? n : (int)std::floor(frac_h[c] * (double)n);
+      if (next_len_h) h = std::min(h, next_len_h[c]);
+      parent_rows_h[c] = row;
+      new_len_h[c] = lens_h[s] + h;
+      head_h[c] = h;
+    } else {
+      parent_rows_h[c] = s;
+      new_len_h[c] = lens_h[s];
+      head_h[c] = 0;
+    }
+  }
   return TTS_OK;
 }
 

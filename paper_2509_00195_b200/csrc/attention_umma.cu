@@ -134,6 +134,8 @@ struct UParams {
   float* partial;             // [2 * gridDim.x][m 128 | l 128 | O 128 x 128]: split tiles' partial states
   int32_t* tile_cnt;          // [n_tiles] pieces of a split tile done (reset by its merger)
   int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
+  int round_robin;            // beam b of a group -> lane quadrant b % 4 (else blocks of consecutive beams)
+  int split_partial_round;    // a last partial round of tiles goes through stream-K (else whole if >= 3/4 full)
   int64_t num_pages;
   float scale_log2;
 };
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // whole-tile rounds (phase 1); a last round that would fill >= 3/4 of the
   // CTAs is also taken whole (cheaper than splitting and merging every tile)
   int k1 = T / Cg;
-  if (4 * (T - k1 * Cg) >= 3 * Cg) ++k1;
+  if (4 * (T - k1 * Cg) >= 3 * Cg && !p.split_partial_round) ++k1;
   const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   auto group_of = [&](int gi) { return p.groups ? p.groups[gi] : inl.g[gi]; };
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -400,10 +402,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   // per beam (host: bpw * G <= 32).  A page's exponentials are computed only
   // by the warps holding one of its member beams, so spreading the beams
   // evenly spreads the softmax work of private pages over all four warps.
+  const bool kRoundRobin = p.round_robin != 0;
   auto row_of = [&](const GroupDesc& g, int row, int& beam, int& head) {
     const int bpw = (g.nbeams + 3) >> 2;
     const int l = row & 31, bw = l / G;
-    beam = (row >> 5) * bpw + bw;
+    beam = kRoundRobin ? bw * 4 + (row >> 5) : (row >> 5) * bpw + bw;
     head = l - bw * G;
     return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
   };
@@ -1117,6 +1120,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.tile_cnt = c->ws_tile_cnt;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.round_robin = c->env_round_robin;
+  p.split_partial_round = c->env_split_partial;
   UInline inl;  // host staging of the parameter block (copied by the launch)
   if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {
     std::memcpy(inl.g, groups_h, (size_t)n_groups * sizeof(GroupDesc));

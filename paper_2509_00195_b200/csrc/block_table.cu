@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_policy(DevState s, const
 // atomics).  Old rows [0, n_old), new rows [0, n_new); n_old > n_new when
 // migrated lineages were imported into spare slots (multi-GPU, a8).
 __global__ void k_fork_count(DevState s, const int32_t* reqs, const int32_t* parent, int n_old, int n_new,
-                             int32_t* tmp_tables, int32_t* tmp_lens) {
+                             int32_t* tmp_tables, int32_t* tmp_lens, const int32_t* new_lens) {
   if (*(volatile int32_t*)s.status) return;
   const int call = blockIdx.y;
   const int b = blockIdx.x;  // old row b and/or new row c = b
@@ -402,7 +402,9 @@ __global__ void k_fork_count(DevState s, const int32_t* reqs, const int32_t* par
   }
   if (b < n_new) {
     const int32_t par = parent[(int64_t)call * s.maxB + b];
-    const int len_par = s.lens[(int64_t)req * s.maxB + par];
+    // (a truncating fork -- speculative beam extension -- keeps only the first
+    // new_lens[b] tokens of the parent row)
+    const int len_par = new_lens ? new_lens[b] : s.lens[(int64_t)req * s.maxB + par];
     const int np_new = (len_par + s.P - 1) / s.P;
     const int32_t* par_row = s.tables + row_base(s, req, par);
     int32_t* new_row = tmp_tables + row_base(s, req, b);
@@ -412,6 +414,46 @@ __global__ void k_fork_count(DevState s, const int32_t* reqs, const int32_t* par
       atomicAdd(&s.ref[p], 1);
     }
     if (threadIdx.x == 0) tmp_lens[(int64_t)req * s.maxB + b] = len_par;
+  }
+}
+
+// Speculative branches (f1): row dst[i] = a copy of row src[i] of request req
+// (table entries, length), one more reference on every page; a partially
+// filled last page is then replaced by a copy (k_alloc cow items, C6).
+__global__ void k_branch_rows(DevState s, int req, const int32_t* __restrict__ src, const int32_t* __restrict__ dst) {
+  if (*(volatile int32_t*)s.status) return;
+  const int i = blockIdx.x;
+  const int a = src[i], b = dst[i];
+  const int len = s.lens[(int64_t)req * s.maxB + a];
+  const int np = (len + s.P - 1) / s.P;
+  const int32_t* from = s.tables + row_base(s, req, a);
+  int32_t* to = s.tables + row_base(s, req, b);
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const int32_t p = from[k];
+    to[k] = p;
+    atomicAdd(&s.ref[p], 1);
+  }
+  if (threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + b] = len;
+}
+
+// Zero token slots [ntok, P) of a row's page (every layer, kv head): the kept
+// last page of a truncated row holds no stale tokens past the row's length.
+// items: (req, row, page position, ntok).
+__global__ void k_zero_tail(DevState s, const int4* items) {
+  if (*(volatile int32_t*)s.status) return;
+  const int4 q = items[blockIdx.x];
+  const int l = blockIdx.y;
+  struct {
+    int32_t dst, ntok;
+  } it{s.tables[row_base(s, q.x, q.y) + q.z], q.w};
+  const int vec_per_row = s.d / 8;
+  const int per_head = s.P * vec_per_row;
+  for (int i = threadIdx.x; i < s.Hkv * per_head; i += blockDim.x) {
+    const int kh = i / per_head, off = i % per_head;
+    if (off < it.ntok * vec_per_row) continue;
+    const int64_t dst = (((int64_t)l * s.num_pages + it.dst) * s.Hkv + kh) * s.P * vec_per_row + off;
+    reinterpret_cast<uint4*>(s.k_pool)[dst] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(s.v_pool)[dst] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -635,13 +677,29 @@ cudaError_t launch_select_policy(Ctx* c, int n_req, const float* scores, int N, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t st) {
+cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t st,
+                               const int32_t* new_lens_d) {
   DevState s = dev_state(c);
   dim3 grid(n_old > n_new ? n_old : n_new, n_req);
-  k_fork_count<<<grid, 128, 0, st>>>(s, reqs_d, c->ws_parent, n_old, n_new, c->ws_tmp_tables, c->ws_tmp_lens);
+  k_fork_count<<<grid, 128, 0, st>>>(s, reqs_d, c->ws_parent, n_old, n_new, c->ws_tmp_tables, c->ws_tmp_lens,
+                                     new_lens_d);
   k_fork_free<<<grid, 128, 0, st>>>(s, reqs_d, n_old);
   k_fork_commit<<<grid, 128, 0, st>>>(s, reqs_d, n_old, n_new, c->ws_tmp_tables, c->ws_tmp_lens);
   c->launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_branch_rows(Ctx* c, int req, const int32_t* src_d, const int32_t* dst_d, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_branch_rows<<<n, 128, 0, st>>>(dev_state(c), req, src_d, dst_d);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_tail(Ctx* c, const int32_t* items_d, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_zero_tail<<<dim3(n, c->cfg.num_layers), 256, 0, st>>>(dev_state(c), (const int4*)items_d);
+  c->launches++;
   return cudaGetLastError();
 }
 

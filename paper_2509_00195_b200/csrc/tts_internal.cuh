@@ -107,6 +107,8 @@ struct Ctx {
   int env_poly = 0;           // TTS_POLY=1: polynomial exp2 for every other pair, 2: for all
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
+  int env_round_robin = 0;    // TTS_ROUND_ROBIN=1: beam b of a group on lane quadrant b % 4
+  int env_split_partial = 0;  // TTS_SPLIT_PARTIAL=1: a partial last round of tiles goes through stream-K
   int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
   // multi-GPU (span.cu)
   Comm* comm = nullptr;
@@ -164,7 +166,10 @@ cudaError_t launch_select(Ctx* c, const int32_t* reqs_d, int n_req, const float*
                           int N, int M, int32_t* parent_out, cudaStream_t s);
 cudaError_t launch_select_policy(Ctx* c, int n_req, const float* scores, int N, int policy, int param,
                                  int32_t* parent_out, cudaStream_t s);
-cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t s);
+cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_old, int n_new, cudaStream_t s,
+                               const int32_t* new_lens_d = nullptr);
+cudaError_t launch_branch_rows(Ctx* c, int req, const int32_t* src_d, const int32_t* dst_d, int n, cudaStream_t s);
+cudaError_t launch_zero_tail(Ctx* c, const int32_t* items_d, int n, cudaStream_t s);  // (req, row, pos, ntok)
 cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t s);
 cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t s);
 cudaError_t launch_select_global(Ctx* c, const float* scores_all, int N, int M, int32_t* parent_out,

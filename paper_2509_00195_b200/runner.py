@@ -75,12 +75,13 @@ class Inputs:
         v = rng.kv_prompt_values(c.seed, "v", l, req, pos, h, c.d, device=self.dev)
         return k.contiguous().to(self.out_dev), v.contiguous().to(self.out_dev)
 
-    def step(self, t: int, greqs: Sequence[int]):
-        """q [L][n][N][Hq][d], k/v [L][n][N][Hkv][d] for global requests greqs."""
+    def step(self, t: int, greqs: Sequence[int], rows: Optional[int] = None):
+        """q [L][n][rows][Hq][d], k/v [L][n][rows][Hkv][d] for global requests greqs
+        (rows = beam slots, default N; row b keyed as beam b)."""
         c = self.cfg
         l = self._idx(c.L, 0, 4)
         r = torch.tensor(list(greqs), device=self.dev).view(1, -1, 1, 1)
-        b = self._idx(c.N, 2, 4)
+        b = self._idx(rows or c.N, 2, 4)
         hq = self._idx(c.Hq, 3, 4)
         hk = self._idx(c.Hkv, 3, 4)
         q = rng.q_values(c.seed, l, r, t, b, hq, c.d, c.q_scale, device=self.dev)
@@ -155,3 +156,107 @@ class BeamStepRunner:
                 if on_fork is not None:
                     on_fork(it, {r: parent[i].cpu().numpy() for i, r in enumerate(greqs)})
         return beam_steps
+
+
+class SpecBeamRunner:
+    """The serving loop of Speculative Beam Extension (Alg. 1, decode
+    side; include/tts.h f1) over libtts: per iteration one decode call over
+    every request's originals still in their step plus its speculative
+    branches; tts_spec_select / tts_spec_branch fill the slots finished beams
+    free (from the second step on: the selection needs a previous score); at
+    a request's step end, selection over the N original scores
+    (tts_beam_select_global), tts_spec_plan and tts_beam_fork_map_trunc.  The
+    bookkeeping here is the loop's (remaining tokens per beam, branch token
+    counts); every decision is libtts's.  spec=False runs the same loop
+    without speculation (the baseline of the same workload)."""
+
+    def __init__(self, cfg: workload.Config, spec: bool = True, R_mean: float = 0.85, R_sigma: float = 0.1,
+                 device: int = 0, num_pages: Optional[int] = None, gen_device=None, lengths=None, scores_fn=None):
+        self.cfg, self.spec = cfg, spec
+        self.R_mean, self.R_sigma = R_mean, R_sigma
+        self.maxB = 2 * cfg.N
+        pages = num_pages or (cfg.R * 2 * cfg.N * workload.max_pages_per_beam(cfg) + 64)
+        self.tcfg = tts_config(cfg, cfg.R, num_pages=pages, max_beams=self.maxB)
+        self.ctx = Context(self.tcfg, device)
+        self.dev = self.ctx.device
+        self.inputs = Inputs(cfg, self.dev, gen_device)
+        self.scale = 1.0 / math.sqrt(cfg.d)
+        self.lengths = workload.step_lengths(cfg) if lengths is None else np.asarray(lengths)
+        self.scores_fn = scores_fn
+
+    def run(self, on_iter: Optional[Callable] = None, on_fork: Optional[Callable] = None) -> dict:
+        """on_iter(t, reqs, rows {r: [rows running]}, out) after each decode call;
+        on_fork(t, r, parent, parent_rows, new_lens) after each fork.  Returns
+        {iterations, running[], capacity[], beam_steps, spec_tokens}."""
+        from . import tts as T
+        c = self.cfg
+        L = self.lengths
+        st = {}
+        for r in range(c.R):
+            k, v = self.inputs.prompt_kv(r)
+            self.ctx.tts_block_table_init_request(r, c.N, c.prompt, k, v)
+            st[r] = {"s": 0, "rem": [int(x) for x in L[r, 0]], "last": None, "k": [0] * c.N, "br": []}
+        stats = {"iterations": 0, "running": [], "capacity": [], "beam_steps": 0, "spec_tokens": 0}
+        parent_d = torch.empty(c.N, dtype=torch.int32, device=self.dev)
+        t = 0
+        while st:
+            reqs = sorted(st)
+            act = np.zeros((len(reqs), self.maxB), dtype=np.uint8)
+            rows_of = {}
+            for i, r in enumerate(reqs):
+                S = st[r]
+                rows = [b for b in range(c.N) if S["rem"][b] > 0] + [c.N + j for j in range(len(S["br"]))]
+                act[i, rows] = 1
+                rows_of[r] = rows
+            q, k, v = self.inputs.step(t, reqs, self.maxB)
+            out = torch.empty(c.L, len(reqs), self.maxB, c.Hq, c.d, dtype=torch.float32, device=self.dev)
+            self.ctx.tts_decode_step(reqs, act, k, v, q, self.scale, out)
+            stats["running"].append(int(act.sum()))
+            stats["capacity"].append(c.N * len(reqs))
+            for r in reqs:
+                S = st[r]
+                for b in range(c.N):
+                    if S["rem"][b] > 0:
+                        S["rem"][b] -= 1
+                        stats["beam_steps"] += 1
+                S["br"] = [(src, n + 1) for src, n in S["br"]]
+                stats["spec_tokens"] += len(S["br"])
+            if on_iter is not None:
+                on_iter(t, reqs, rows_of, out)
+            for r in reqs:
+                S = st[r]
+                if all(x == 0 for x in S["rem"]):
+                    s = S["s"]
+                    if s + 1 >= c.n_steps:
+                        self.ctx.tts_block_table_release_request(r)
+                        del st[r]
+                        continue
+                    sc = (torch.as_tensor(list(self.scores_fn(r, s)), dtype=torch.float32, device=self.dev)
+                          if self.scores_fn else self.inputs.scores(r, s))
+                    self.ctx.tts_beam_select_global(sc.contiguous(), c.M, parent_d)
+                    parent = parent_d.cpu().tolist()
+                    lens = list(self.ctx.tts_seq_lens_host(r)[: c.N])
+                    frac = [rng.truncation_fraction(c.seed, r, s, ch, self.R_mean, self.R_sigma) for ch in range(c.N)]
+                    nxt = [int(x) for x in L[r, s + 1]]
+                    prow, nlen, head = T.spec_plan(parent, c.M, S["br"], lens, frac, nxt)
+                    self.ctx.tts_beam_fork_map_trunc(r, prow, nlen)
+                    if on_fork is not None:
+                        on_fork(t, r, parent, prow, nlen)
+                    scl = sc.cpu().tolist()
+                    S.update(s=s + 1, rem=[nxt[ch] - head[ch] for ch in range(c.N)],
+                             last=[scl[parent[ch]] for ch in range(c.N)], k=[0] * c.N, br=[])
+                elif self.spec and S["last"] is not None:
+                    free = c.N - sum(1 for x in S["rem"] if x > 0) - len(S["br"])
+                    cand = [b for b in range(c.N) if S["rem"][b] == 0]
+                    if cand and free > 0:
+                        add = T.spec_select(cand, [S["last"][b] for b in cand], [S["k"][b] for b in cand], free, c.M)
+                        src = []
+                        for b, n in zip(cand, add):  # branch rows in ascending source beam order
+                            src += [b] * n
+                            S["k"][b] += n
+                        if src:
+                            self.ctx.tts_spec_branch(r, src)
+                            S["br"] += [(b, 0) for b in src]
+            t += 1
+        stats["iterations"] = t
+        return stats

@@ -103,6 +103,10 @@ def load() -> ctypes.CDLL:
             "tts_span_gids": [_P, _I, _P],
             "tts_beam_select_fork_global": [_P, _I, _P, _I, _P, _P, _P],
             "tts_span_placement": [_I, _P, _P, _I, _P, _P],
+            "tts_spec_select": [_I, _P, _P, _P, _I, _I, _P],
+            "tts_spec_branch": [_P, _I, _I, _P, _P],
+            "tts_spec_plan": [_I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+            "tts_beam_fork_map_trunc": [_P, _I, _I, _P, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -141,6 +145,30 @@ def span_placement(parent_gid: Sequence[int], old_rank: Sequence[int], caps: Seq
     _check(load().tts_span_placement(n, _i32_host(parent_gid), _i32_host(old_rank), len(caps), _i32_host(caps),
                                      out), "tts_span_placement")
     return list(out)
+
+
+def spec_select(beams: Sequence[int], last_scores: Sequence[float], have: Sequence[int], free_slots: int,
+                B: int) -> list:
+    """tts_spec_select (host only): new speculative branches per candidate."""
+    n = len(beams)
+    sc = (ctypes.c_float * max(1, n))(*[float(x) for x in last_scores])
+    out = (_I * max(1, n))()
+    _check(load().tts_spec_select(n, _i32_host(beams), sc, _i32_host(have), int(free_slots), int(B), out),
+           "tts_spec_select")
+    return list(out)[:n]
+
+
+def spec_plan(parent: Sequence[int], M: int, branches: Sequence, lens: Sequence[int], frac: Sequence[float],
+              next_len: Optional[Sequence[int]] = None):
+    """tts_spec_plan (host only): (parent_rows, new_lens, head) of DuplicateThenTruncate."""
+    N = len(parent)
+    nb = len(branches)
+    fr = (ctypes.c_double * N)(*[float(x) for x in frac])
+    pr, nl, hd = (_I * N)(), (_I * N)(), (_I * N)()
+    _check(load().tts_spec_plan(N, int(M), _i32_host(parent), nb, _i32_host([b[0] for b in branches] or [0]),
+                                _i32_host([b[1] for b in branches] or [0]), _i32_host(lens), fr,
+                                None if next_len is None else _i32_host(next_len), pr, nl, hd), "tts_spec_plan")
+    return list(pr), list(nl), list(hd)
 
 
 def stream_read_gbs(buf: torch.Tensor, iters: int = 10) -> float:
@@ -309,6 +337,14 @@ class Context:
     def tts_beam_fork_map(self, req, parent_local):
         arr = _i32_host(parent_local)
         _check(self.lib.tts_beam_fork_map(self.h, req, len(parent_local), arr, self.stream), "tts_beam_fork_map")
+
+    def tts_spec_branch(self, req, src_rows):
+        _check(self.lib.tts_spec_branch(self.h, req, len(src_rows), _i32_host(src_rows), self.stream),
+               "tts_spec_branch")
+
+    def tts_beam_fork_map_trunc(self, req, parent_rows, new_lens):
+        _check(self.lib.tts_beam_fork_map_trunc(self.h, req, len(parent_rows), _i32_host(parent_rows),
+                                                _i32_host(new_lens), self.stream), "tts_beam_fork_map_trunc")
 
     def tts_lineage_bytes(self, length) -> int:
         n = ctypes.c_size_t()

@@ -27,6 +27,7 @@ STREAM_K_PROMPT = 4
 STREAM_V_PROMPT = 5
 STREAM_SCORE = 6
 STREAM_STEPLEN = 7
+STREAM_TRUNC = 8
 
 
 def _mul32(x: torch.Tensor, c: int) -> torch.Tensor:
@@ -109,3 +110,15 @@ def score_values_fine(seed, req, step, beam, device="cpu") -> torch.Tensor:
     """Unquantised variant: U[0,1) with 24 random bits (exact in fp32)."""
     u = uniform_u32((seed, STREAM_SCORE, req, step, beam), device)
     return ((u >> 8).to(torch.float32) / float(1 << 24))
+
+
+def truncation_fraction(seed, req, step, child, mean: float, sigma: float) -> float:
+    """Speculative-token truncation fraction f ~ Normal(mean, sigma) clamped to
+    [0, 1] for child `child` of the fork after TTS step `step` (PAPER.md P:311
+    "drawn from a normal distribution with mean R"; SPEC S:67 sigma 0.1): a
+    random input of DuplicateThenTruncate, drawn here once (float64, Box-Muller
+    on two counter-based uniforms) and handed to both the oracle and libtts."""
+    import math
+    u = [(int(uniform_u32((seed, STREAM_TRUNC, req, step, child, k))) + 0.5) / 4294967296.0 for k in (1, 2)]
+    z = math.sqrt(-2.0 * math.log(u[0])) * math.cos(2.0 * math.pi * u[1])
+    return min(1.0, max(0.0, mean + sigma * z))
