@@ -200,22 +200,26 @@ class SpecRun:
         self.scores_fn = scores_fn      # (r, s) -> N scores (default: synth's)
 
     def _output(self, r: int, row: int, t: int, l: int) -> np.ndarray:
+        """fp64 attention of row `row` over its own token list (read through its
+        table), K/V regenerated from the token identities."""
         from synth import rng
         from .attention import attention_fp64
         import torch
         c = self.cfg
         ident = self.sim.gather(r, row)
-        kv = [x for x in ident]
-        K = np.empty((len(kv), c.Hkv, c.d))
+        K = np.empty((len(ident), c.Hkv, c.d))
         V = np.empty_like(K)
-        kvh = torch.arange(c.Hkv)
-        for i, tok in enumerate(kv):
-            if tok[0] == "p":
-                K[i] = self.kv.prompt(r, l, "k")[tok[2]].double().numpy()
-                V[i] = self.kv.prompt(r, l, "v")[tok[2]].double().numpy()
-            else:
-                K[i] = rng.kv_decode_values(c.seed, "k", l, r, tok[2], tok[3], kvh, c.d).double().numpy()
-                V[i] = rng.kv_decode_values(c.seed, "v", l, r, tok[2], tok[3], kvh, c.d).double().numpy()
+        kvh = torch.arange(c.Hkv).view(1, -1)
+        ip = [i for i, tok in enumerate(ident) if tok[0] == "p"]
+        idd = [i for i, tok in enumerate(ident) if tok[0] != "p"]
+        if ip:
+            K[ip] = self.kv.prompt(r, l, "k")[[ident[i][2] for i in ip]].double().numpy()
+            V[ip] = self.kv.prompt(r, l, "v")[[ident[i][2] for i in ip]].double().numpy()
+        if idd:
+            tt = torch.tensor([ident[i][2] for i in idd]).view(-1, 1)
+            bb = torch.tensor([ident[i][3] for i in idd]).view(-1, 1)
+            K[idd] = rng.kv_decode_values(c.seed, "k", l, r, tt, bb, kvh, c.d).double().numpy()
+            V[idd] = rng.kv_decode_values(c.seed, "v", l, r, tt, bb, kvh, c.d).double().numpy()
         q = rng.q_values(c.seed, l, r, t, row, torch.arange(c.Hq), c.d, c.q_scale).double().numpy()
         return attention_fp64(q, K, V, 1.0 / math.sqrt(c.d))
 

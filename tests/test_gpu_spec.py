@@ -80,7 +80,7 @@ def test_spec_parity(seed, d, G, N, M, R):
 def test_spec_equivalence_and_occupancy_on_gpu():
     """Same survivors with speculation on and off; higher slot occupancy and
     no more iterations with it (C4-shaped straggler steps, 1.5B heads)."""
-    cfg = workload.C4.with_(R=2, N=32, n_steps=3, L=1, ln_cap=400)
+    cfg = workload.C4.with_(R=2, N=16, n_steps=3, L=1, ln_cap=300)
     on_tr, on = _parity(cfg, True, every=97)
     off_tr, off = _parity(cfg, False, every=97)
     assert [f["parent"] for f in on_tr.forks] == [f["parent"] for f in off_tr.forks]
