@@ -224,6 +224,24 @@ tts_status_t tts_beam_select_fork_policy(tts_ctx_t ctx, int32_t n_req, const int
                                          const float* scores, int32_t policy, int32_t param,
                                          int32_t* parent_out, void* stream);
 
+/* f3. Dynamic Prefix-Aware Scheduling under a memory budget (PAPER.md 4.2,
+ * P:372-394; Appendix A; DESIGN.md ledger C30).  Schedules the beams of request
+ * req (active_h: host uint8 [n_beams], NULL = all) for execution in batches
+ * ("tries") under a KV budget of budget_pages pages: CoT = a beam's page list,
+ * P(a, b) = shared leading pages; greedy order (order[0] = the first beam,
+ * then the unscheduled beam with the largest P with its predecessor, ties to
+ * the lower index -- for the DFS-ordered rows of ledger C5 P(a, b) is the
+ * minimum of the adjacent rows' shared prefixes between a and b), tries =
+ * consecutive beams of the order packed first-fit while their union of pages
+ * fits the budget.  Outputs: order_h [n] (beam ids), trie_of_h [n_beams]
+ * (trie of each scheduled beam), *n_tries_h, *cost_h = sum_i (Nodes(T_i) -
+ * P(T_i, T_{i+1})) and *shared_h = sum_i P(T_i, T_{i+1}) in pages, P(T_last,.)
+ * = 0 -- the pages a memory-bounded server evicts and recomputes per pass over
+ * the beams.  Syncs (reads the request's tables). */
+tts_status_t tts_dpas_plan(tts_ctx_t ctx, int32_t req, int64_t budget_pages, const uint8_t* active_h,
+                           int32_t* order_h, int32_t* trie_of_h, int32_t* n_tries_h, int64_t* cost_h,
+                           int64_t* shared_h, void* stream);
+
 /* ---- f1: Speculative Beam Extension, decode side (PAPER.md 4.1, Alg. 1
  * P:324-350; DESIGN.md ledger C25-C29) ------------
  * While the stragglers of a step still generate, the slots of finished beams

@@ -897,6 +897,113 @@ tts_status_t tts_block_table_snapshot(tts_ctx_t c, int32_t req, int32_t* n_beams
   return TTS_OK;
 }
 
+// f3: Dynamic Prefix-Aware Scheduling under a memory budget (PAPER.md 4.2,
+// Appendix A).  Host scheduler over the request's device tables (one
+// snapshot): CoT = a beam's page list; P(a, b) = shared leading pages, which
+// for rows in DFS order (ledger C5) is the minimum of the adjacent rows'
+// shared prefixes between them (the beam tree is prefix-closed).
+tts_status_t tts_dpas_plan(tts_ctx_t c, int32_t req, int64_t budget_pages, const uint8_t* active_h,
+                           int32_t* order_h, int32_t* trie_of_h, int32_t* n_tries_h, int64_t* cost_h,
+                           int64_t* shared_h, void* stream) {
+  if (!c || !order_h || !trie_of_h || !n_tries_h || !cost_h || !shared_h || budget_pages <= 0)
+    return TTS_ERR_INVALID_ARG;
+  if (!installed(c, req)) return TTS_ERR_STATE;
+  const tts_config_t& g = c->cfg;
+  const int P = g.page_size;
+  const int N = c->n_beams[req];
+  std::vector<int32_t> tab((size_t)N * g.max_pages_per_beam);
+  cudaStream_t st = (cudaStream_t)stream;
+  TTS_CUDA(cudaMemcpyAsync(tab.data(), c->buf.block_tables + entry_of(g, req, 0, 0), tab.size() * 4,
+                           cudaMemcpyDeviceToHost, st));
+  TTS_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> cots;  // the scheduled beams (active), input = index order
+  for (int b = 0; b < N; ++b)
+    if (!active_h || active_h[b]) cots.push_back(b);
+  const int n = (int)cots.size();
+  *n_tries_h = 0;
+  *cost_h = 0;
+  *shared_h = 0;
+  if (n == 0) return TTS_OK;
+  auto np = [&](int i) { return (c->lens[(int64_t)req * g.max_beams + cots[i]] + P - 1) / P; };
+  auto row = [&](int i) { return tab.data() + (size_t)cots[i] * g.max_pages_per_beam; };
+  std::vector<int> adj(n, 0);  // adj[i] = P(cot i, cot i+1)
+  for (int i = 0; i + 1 < n; ++i) {
+    const int m = std::min(np(i), np(i + 1));
+    int k = 0;
+    while (k < m && row(i)[k] == row(i + 1)[k]) ++k;
+    adj[i] = k;
+  }
+  // greedy: the unscheduled CoT with the largest P with the
+  // predecessor, ties to input order; order[0] = the first CoT
+  std::vector<char> used(n, 0);
+  std::vector<int> order;
+  order.push_back(0);
+  used[0] = 1;
+  for (int k = 1; k < n; ++k) {
+    const int prev = order.back();
+    // P(prev, j) for every j by one sweep each way over adj
+    int best = -1, bestp = -1;
+    int m = INT32_MAX;
+    for (int j = prev - 1; j >= 0; --j) {
+      m = std::min(m, adj[j]);
+      if (!used[j] && (m > bestp || (m == bestp && j < best))) best = j, bestp = m;
+    }
+    m = INT32_MAX;
+    for (int j = prev + 1; j < n; ++j) {
+      m = std::min(m, adj[j - 1]);
+      if (!used[j] && (m > bestp || (m == bestp && j < best))) best = j, bestp = m;
+    }
+    order.push_back(best);
+    used[best] = 1;
+  }
+  // first-fit packing into tries of <= budget pages, and the eviction cost
+  std::vector<int32_t> mark((size_t)g.num_pages, -1);
+  std::vector<std::vector<int>> tries;
+  std::vector<int64_t> tsize;
+  int64_t cur = 0;
+  for (int i : order) {
+    int64_t add = 0;
+    for (int k = 0; k < np(i); ++k) add += mark[row(i)[k]] != (int)tries.size() - 1 || tries.empty();
+    if (!tries.empty() && cur + add <= budget_pages) {
+      for (int k = 0; k < np(i); ++k) mark[row(i)[k]] = (int)tries.size() - 1;
+      tries.back().push_back(i);
+      cur += add;
+    } else {
+      tries.push_back({i});
+      cur = 0;
+      for (int k = 0; k < np(i); ++k)
+        if (mark[row(i)[k]] != (int)tries.size() - 1) mark[row(i)[k]] = (int)tries.size() - 1, ++cur;
+    }
+    tsize.resize(tries.size());
+    tsize.back() = cur;
+  }
+  // shared nodes of consecutive tries
+  std::vector<int32_t> seen((size_t)g.num_pages, -1);
+  int64_t shared = 0, nodes = 0;
+  for (size_t t = 0; t < tries.size(); ++t) {
+    nodes += tsize[t];
+    if (t + 1 < tries.size()) {
+      for (int i : tries[t])
+        for (int k = 0; k < np(i); ++k) seen[row(i)[k]] = (int)t;
+      for (int i : tries[t + 1])
+        for (int k = 0; k < np(i); ++k) {
+          const int32_t p = row(i)[k];
+          if (seen[p] == (int)t) {
+            seen[p] = -2 - (int)t;  // count once
+            ++shared;
+          }
+        }
+    }
+  }
+  for (int k = 0; k < n; ++k) order_h[k] = cots[order[k]];
+  for (size_t t = 0; t < tries.size(); ++t)
+    for (int i : tries[t]) trie_of_h[cots[i]] = (int32_t)t;
+  *n_tries_h = (int32_t)tries.size();
+  *cost_h = nodes - shared;
+  *shared_h = shared;
+  return TTS_OK;
+}
+
 tts_status_t tts_block_table_stats(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
                                    const uint8_t* active, int64_t* accum, void* stream) {
   if (!c || n_req <= 0 || !req_ids || !accum) return TTS_ERR_INVALID_ARG;

@@ -106,6 +106,16 @@ class BeamStepRunner:
         self.dev = self.ctx.device
         self.inputs = Inputs(cfg, self.dev, gen_device)
         self.scale = 1.0 / math.sqrt(cfg.d)
+        # f3: decode in DPAS tries under a KV budget (pages; None = one call for all beams)
+        self.dpas_budget: Optional[int] = None
+        self.last_n_tries = 1
+        self._tries = None
+
+    def _plan_tries(self):
+        """DPAS tries of request 0 (the schedule is made once per TTS step,
+        PAPER.md Appendix A.1 assumption 2)."""
+        order, trie_of, nt, _, _ = self.ctx.tts_dpas_plan(0, self.dpas_budget)
+        self._tries = [[b for b in order if trie_of[b] == t] for t in range(nt)]
 
     def install(self):
         for r in self.req_ids:
@@ -132,7 +142,18 @@ class BeamStepRunner:
             active = np.stack(it.active).astype(np.uint8)
             q, k, v = self.inputs.step(it.t, it.reqs)
             out = torch.empty(c.L, n, c.N, c.Hq, c.d, dtype=torch.float32, device=self.dev)
-            if self.fused:
+            if self.dpas_budget is not None:
+                assert len(self.req_ids) == 1 and self.fused, "DPAS batches: one request"
+                if self._tries is None:
+                    self._plan_tries()
+                self.last_n_tries = 0
+                for trie in self._tries:
+                    a = np.zeros_like(active)
+                    a[0, trie] = active[0, trie]
+                    if a.any():
+                        self.ctx.tts_decode_step(loc, a, k, v, q, self.scale, out)
+                        self.last_n_tries += 1
+            elif self.fused:
                 self.ctx.tts_decode_step(loc, active, k, v, q, self.scale, out)
             else:
                 self.ctx.tts_block_table_append(loc, active, k, v)
@@ -153,6 +174,7 @@ class BeamStepRunner:
                 else:
                     self.ctx.tts_beam_select_fork_policy([self.local[r] for r in greqs], sc.contiguous(), policy[0],
                                                          policy[1], parent)
+                self._tries = None  # a new schedule for the next step
                 if on_fork is not None:
                     on_fork(it, {r: parent[i].cpu().numpy() for i, r in enumerate(greqs)})
         return beam_steps

@@ -107,6 +107,7 @@ def load() -> ctypes.CDLL:
             "tts_spec_branch": [_P, _I, _I, _P, _P],
             "tts_spec_plan": [_I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P],
             "tts_beam_fork_map_trunc": [_P, _I, _I, _P, _P, _P],
+            "tts_dpas_plan": [_P, _I, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _P],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -337,6 +338,19 @@ class Context:
     def tts_beam_fork_map(self, req, parent_local):
         arr = _i32_host(parent_local)
         _check(self.lib.tts_beam_fork_map(self.h, req, len(parent_local), arr, self.stream), "tts_beam_fork_map")
+
+    def tts_dpas_plan(self, req, budget_pages, active=None):
+        """-> (order, trie_of [n_beams], n_tries, cost, shared)."""
+        n = self.n_beams(req)
+        order = (_I * n)()
+        trie = (_I * n)(*([-1] * n))
+        nt = ctypes.c_int32()
+        cost, shared = ctypes.c_int64(), ctypes.c_int64()
+        _a, ap = _u8_host(active)
+        _check(self.lib.tts_dpas_plan(self.h, req, int(budget_pages), ap, order, trie, ctypes.byref(nt),
+                                      ctypes.byref(cost), ctypes.byref(shared), self.stream), "tts_dpas_plan")
+        k = n if active is None else int(np.asarray(active).astype(bool).sum())
+        return list(order)[:k], list(trie), nt.value, cost.value, shared.value
 
     def tts_spec_branch(self, req, src_rows):
         _check(self.lib.tts_spec_branch(self.h, req, len(src_rows), _i32_host(src_rows), self.stream),

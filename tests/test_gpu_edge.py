@@ -175,3 +175,62 @@ def test_c5_full_chains_n64_slice():
     cfg = workload.C5.with_(N=64, L=1)
     res = run_parity(cfg, _sparse(cfg, [0, 33, 63], [0], 1021), check_refs=False)
     assert res["n_forks"] == 31
+
+
+@pytest.mark.parametrize("name,budgets", [("C2", [16, 40, 160, 10 ** 6]), ("C3", [64, 400, 2000])])
+def test_dpas_plan_and_batched_decode(name, budgets):
+    """f3: tts_dpas_plan on the device tables equals the oracle's greedy
+    schedule, first-fit tries and eviction cost (oracle/dpas.py, pinned to
+    SPEC S:150-199 and Appendix A) at every fork; decoding the beams trie by
+    trie (one call per trie, as a memory-bounded server would) gives the same
+    outputs within 2e-3 of the oracle."""
+    from oracle.dpas import eviction_cost, greedy_schedule, pack_tries
+    from paper_2509_00195_b200.runner import BeamStepRunner
+    cfg = workload.CONFIGS[name].with_(n_steps=3, step_len=64, L=2)
+    pages = default_num_pages(cfg, 1)
+    orc = OracleRun(cfg, num_pages=pages, track_content=False)
+    plans = []
+
+    def on_fork_orc(run, rec):
+        cots = [list(row) for row in run.sim.tables[0]]
+        g = greedy_schedule(cots)
+        for bud in budgets:
+            tries = pack_tries(g, cots, bud)
+            cost, shared = eviction_cost(tries, cots)
+            plans.append((g, tries, cost, shared))
+
+    orc.run(on_fork=on_fork_orc, snapshot_refs=False)
+    runner = BeamStepRunner(cfg, num_pages=pages, gen_device="cpu")
+    got = []
+
+    def on_fork(it, parents):
+        for bud in budgets:
+            order, trie_of, nt, cost, shared = runner.ctx.tts_dpas_plan(0, bud)
+            tries = [[b for b in order if trie_of[b] == t] for t in range(nt)]
+            got.append((order, tries, cost, shared))
+
+    runner.run(on_fork=on_fork)
+    assert got == plans and len(got) == (cfg.n_steps - 1) * len(budgets)
+
+
+def test_dpas_batched_decode_matches_oracle():
+    from paper_2509_00195_b200.runner import BeamStepRunner
+    cfg = workload.C2.with_(n_steps=3, step_len=40, L=2)
+    sample = _sparse(cfg, range(cfg.N), range(cfg.L), 7)
+    orc = OracleRun(cfg, num_pages=default_num_pages(cfg, 1), track_content=False)
+    tr = orc.run(sample=sample, snapshot_refs=False)
+    runner = BeamStepRunner(cfg, num_pages=default_num_pages(cfg, 1), gen_device="cpu")
+    runner.dpas_budget = 24  # pages: a few beams per trie
+    outs = {}
+    seen_tries = []
+
+    def on_iter(it, out, active):
+        for (r, b, l) in sample(it):
+            outs[(it.t, r, b, l)] = out[l, 0, b].double().cpu().numpy()
+        seen_tries.append(runner.last_n_tries)
+
+    runner.run(on_iter=on_iter)
+    assert max(seen_tries) > 1
+    for key, ref in tr.outputs.items():
+        e = float((np.abs(outs[key] - ref).max(-1) / np.abs(ref).max(-1)).max())
+        assert e <= 2e-3, (key, e)
