@@ -378,6 +378,7 @@ class SpanBench:
         from paper_2509_00195_b200.runner import tts_config, Inputs, pages_per_request
         from paper_2509_00195_b200.tts import Context
         self.cfg, self.world, self.rank = cfg, world, rank
+        self.dedup = os.environ.get("TTS_SPAN_DEDUP", "1") != "0"  # f4: cross-GPU page deduplication
         self.nl = cfg.N // world
         maxb = 2 * self.nl if world > 1 else cfg.N
         if world == 1:
@@ -423,7 +424,7 @@ class SpanBench:
         self._chk(lib.tts_block_table_init_request(h, 0, self.nl, c.prompt, k.data_ptr(), v.data_ptr(), st), "init")
         if self.world > 1:
             from paper_2509_00195_b200.dist import equal_caps
-            self.ctx.tts_span_init(0, c.N, equal_caps(c.N, self.world))
+            self.ctx.tts_span_init(0, c.N, equal_caps(c.N, self.world), self.dedup)
         nr = len(self.ring)
         open_ev = None
         for it in self.sched:

@@ -396,7 +396,16 @@ tts_status_t tts_comm_destroy(tts_ctx_t ctx);
  * contiguous global ids [sum(caps[:rank]), sum(caps[:rank+1])) -- at install
  * every beam holds only the prompt, so the cut is byte-balanced.  The request
  * must have been installed with caps_h[rank] beams. */
-tts_status_t tts_span_init(tts_ctx_t ctx, int32_t req, int32_t n_global, const int32_t* caps_h);
+tts_status_t tts_span_init(tts_ctx_t ctx, int32_t req, int32_t n_global, const int32_t* caps_h, int32_t dedup);
+
+/* f4 (extends 8(e)): with dedup != 0 in tts_span_init the context
+ * tracks every page's origin (who created it, where; equal on every rank
+ * holding a copy).  A migrating lineage then crosses only the tokens past the
+ * longest run of leading full pages some beam of the destination already
+ * holds (same origins; ties to the lowest gid): the destination references
+ * that beam's pages for the prefix and receives the rest.  Bytes this rank
+ * sent and did not need to send, summed over the request's forks: */
+tts_status_t tts_span_stats(tts_ctx_t ctx, int32_t req, int64_t* migrated_bytes_h, int64_t* deduped_bytes_h);
 
 /* Global ids of this rank's rows of a spanning request (host int32 [n_local]). */
 tts_status_t tts_span_gids(tts_ctx_t ctx, int32_t req, int32_t* gids_h);

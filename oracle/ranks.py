@@ -24,6 +24,11 @@ module writes out plainly:
   copy-on-write of a partially filled last page for every child but the first
   (in new-row order) of the same parent (C6-C8).
 * page ids are per rank (each rank has its own allocator, C20).
+* f4, cross-GPU deduplication (an extension of 8(e); DESIGN.md ledger C31):
+  an imported lineage reuses the longest run of its leading FULL pages that
+  one of the destination's pre-fork beams holds with the same tokens (ties to
+  the lowest gid): the imported row references that beam's first m pages and
+  allocates only the remaining ones.
 """
 from __future__ import annotations
 
@@ -77,18 +82,22 @@ def rank_plans(parent_gid: Sequence[int], old_gids: Sequence[Sequence[int]], chi
 class RankSim(BlockTableSim):
     """BlockTableSim plus the two operations of a spanning fork."""
 
-    def import_lineage(self, req: int, row: int, ident: Sequence) -> None:
+    def import_lineage(self, req: int, row: int, ident: Sequence, share_row: int = -1, m: int = 0) -> None:
         P = self.P
         n = len(ident)
-        pages = [self._alloc() for _ in range(-(-n // P))]
+        shared = list(self.tables[req][share_row][:m]) if m else []
+        for p in shared:
+            self.ref[p] += 1
+        pages = [self._alloc() for _ in range(-(-n // P) - m)]
         for p in pages:
             self.ref[p] = 1
         if self.track:
             for i, tok in enumerate(ident):
-                self.content[pages[i // P]][i % P] = tok
+                if i >= m * P:
+                    self.content[pages[i // P - m]][i % P] = tok
         rows, lens = self.tables[req], self.lens[req]
         assert row == len(rows)
-        rows.append(pages)
+        rows.append(shared + pages)
         lens.append(n)
 
     def fork_map(self, req: int, parent_rows: Sequence[int]) -> None:
@@ -138,10 +147,13 @@ class SpanModel:
     gid activity, fork by gid-indexed scores)."""
 
     def __init__(self, N: int, caps: Sequence[int], num_pages: int, P: int, prompt_len: int,
-                 req: int = 0, track_content: bool = True):
+                 req: int = 0, track_content: bool = True, dedup: bool = False):
         assert sum(caps) == N
         self.N, self.caps, self.P, self.req = N, list(caps), P, req
         self.G = len(caps)
+        self.dedup = dedup
+        self.migrated_tokens = 0
+        self.deduped_tokens = 0
         self.sims = [RankSim(num_pages, P, track_content) for _ in caps]
         starts = [sum(caps[:r]) for r in range(self.G)]
         self.gids = [list(range(starts[r], starts[r] + caps[r])) for r in range(self.G)]
@@ -188,9 +200,27 @@ class SpanModel:
                 row = self.gids[src].index(p)
                 lineages[p] = sim.gather(self.req, row) if sim.track else [None] * sim.lens[self.req][row]
         rec = SpanFork(parent, child_rank, plans)
+        # f4: the longest run of leading full pages of p that a pre-fork beam
+        # of the destination holds with the same tokens (ties: lowest gid)
+        old_gids = [list(g) for g in self.gids]
+        pre = {g: self.gather(g) for gs in old_gids for g in gs} if self.dedup else {}
         for r, (sim, pl) in enumerate(zip(self.sims, plans)):
             for k, p in enumerate(pl.imports):
-                sim.import_lineage(self.req, len(self.gids[r]) + k, lineages[p])
+                m, share = 0, -1
+                if self.dedup:
+                    for y in old_gids[r]:
+                        lcp = 0
+                        for a, b in zip(lineages[p], pre[y]):
+                            if a != b:
+                                break
+                            lcp += 1
+                        if lcp // self.P > m:
+                            m, share = lcp // self.P, y
+                n = len(lineages[p])
+                self.migrated_tokens += n - m * self.P
+                self.deduped_tokens += m * self.P
+                sim.import_lineage(self.req, len(self.gids[r]) + k, lineages[p],
+                                   old_gids[r].index(share) if m else -1, m)
             sim.fork_map(self.req, pl.parent_rows)
             self.gids[r] = list(pl.children)
         for sim in self.sims:

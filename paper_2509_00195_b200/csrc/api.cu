@@ -339,6 +339,7 @@ tts_status_t tts_block_table_append(tts_ctx_t c, int32_t n_req, const int32_t* r
   if (s != TTS_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
+  tts::span_note_append(c, n_req, req_ids, ap.items);
   if (!ap.items.empty()) TTS_CUDA(tts::launch_alloc_host(c, ap.items.data(), (int)ap.items.size(), st));
   if (!ap.slots.empty()) {
     void* d = tts::upload(c, ap.slots.data(), ap.slots.size() * 4, st, &e);
@@ -529,6 +530,7 @@ tts_status_t tts_decode_step(tts_ctx_t c, int32_t n_req, const int32_t* req_ids,
     return s;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  tts::span_note_append(c, n_req, req_ids, app.items);
   if (!app.items.empty()) TTS_CUDA(tts::launch_alloc_host(c, app.items.data(), (int)app.items.size(), st));
   return attn_launch(c, ap, 0, c->cfg.num_layers, n_req, q, scale, out, stream, &app.slots, k_new, v_new);
 }

@@ -496,16 +496,16 @@ __global__ void k_fork_commit(DevState s, const int32_t* reqs, int n_old, int n_
 
 // Lineage export (migration, a8): the beam's len tokens of every layer as a
 // contiguous bf16 buffer [2 (K, V)][L][len][Hkv][d].  One block per (token, layer).
-__global__ void k_lineage_export(DevState s, int req, int beam, int len, uint4* __restrict__ buf) {
+__global__ void k_lineage_export(DevState s, int req, int beam, int len, int t0, uint4* __restrict__ buf) {
   if (*(volatile int32_t*)s.status) return;
-  const int t = blockIdx.x, l = blockIdx.y;
+  const int t = t0 + blockIdx.x, l = blockIdx.y;
   const int vpr = s.d / 8, n = s.Hkv * vpr;
   const int32_t page = s.tables[row_base(s, req, beam) + t / s.P];
-  const int64_t plane = (int64_t)s.L * len * n;
+  const int64_t plane = (int64_t)s.L * (len - t0) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int kh = i / vpr, e = i % vpr;
     const int64_t src = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + t % s.P) * vpr + e;
-    const int64_t dst = (((int64_t)l * len + t) * s.Hkv + kh) * vpr + e;
+    const int64_t dst = (((int64_t)l * (len - t0) + (t - t0)) * s.Hkv + kh) * vpr + e;
     buf[dst] = reinterpret_cast<const uint4*>(s.k_pool)[src];
     buf[plane + dst] = reinterpret_cast<const uint4*>(s.v_pool)[src];
   }
@@ -513,20 +513,34 @@ __global__ void k_lineage_export(DevState s, int req, int beam, int len, uint4* 
 
 // Lineage import: write the buffer into the beam's freshly allocated pages and
 // set its length (the pages were allocated by k_alloc into the row first).
-__global__ void k_lineage_import(DevState s, int req, int beam, int len, const uint4* __restrict__ buf) {
+__global__ void k_lineage_import(DevState s, int req, int beam, int len, int t0, const uint4* __restrict__ buf) {
   if (*(volatile int32_t*)s.status) return;
-  const int t = blockIdx.x, l = blockIdx.y;  // t < ceil(len / P) * P: slots past len are zeroed
+  const int t = t0 + blockIdx.x, l = blockIdx.y;  // t < ceil(len / P) * P: slots past len are zeroed
   const int vpr = s.d / 8, n = s.Hkv * vpr;
   const int32_t page = s.tables[row_base(s, req, beam) + t / s.P];
-  const int64_t plane = (int64_t)s.L * len * n;
+  const int64_t plane = (int64_t)s.L * (len - t0) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int kh = i / vpr, e = i % vpr;
     const int64_t dst = ((((int64_t)l * s.num_pages + page) * s.Hkv + kh) * s.P + t % s.P) * vpr + e;
-    const int64_t src = (((int64_t)l * len + t) * s.Hkv + kh) * vpr + e;
+    const int64_t src = (((int64_t)l * (len - t0) + (t - t0)) * s.Hkv + kh) * vpr + e;
     reinterpret_cast<uint4*>(s.k_pool)[dst] = t < len ? buf[src] : make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(s.v_pool)[dst] = t < len ? buf[plane + src] : make_uint4(0, 0, 0, 0);
   }
-  if (t == 0 && l == 0 && threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + beam] = len;
+  if (t == t0 && l == 0 && threadIdx.x == 0) s.lens[(int64_t)req * s.maxB + beam] = len;
+}
+
+// Row `beam` of request req takes the first m page entries of local row
+// `share` (one more reference each): the shared prefix of an imported
+// lineage (f4, cross-GPU deduplication).
+__global__ void k_share_prefix(DevState s, int req, int beam, int share, int m) {
+  if (*(volatile int32_t*)s.status) return;
+  const int32_t* from = s.tables + row_base(s, req, share);
+  int32_t* to = s.tables + row_base(s, req, beam);
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const int32_t p = from[k];
+    to[k] = p;
+    atomicAdd(&s.ref[p], 1);
+  }
 }
 
 // Release a request: -1 per entry, then free the pages that reached 0.
@@ -703,18 +717,26 @@ cudaError_t launch_zero_tail(Ctx* c, const int32_t* items_d, int n, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t st) {
-  if (len <= 0) return cudaSuccess;
-  k_lineage_export<<<dim3(len, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len, (uint4*)buf);
+cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t st, int t0) {
+  if (len - t0 <= 0) return cudaSuccess;
+  k_lineage_export<<<dim3(len - t0, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len, t0,
+                                                                      (uint4*)buf);
   c->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t st) {
-  if (len <= 0) return cudaSuccess;
+cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t st, int t0) {
   const int P = c->cfg.page_size;
-  k_lineage_import<<<dim3((len + P - 1) / P * P, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam, len,
-                                                                                  (const uint4*)buf);
+  if ((len + P - 1) / P * P - t0 <= 0) return cudaSuccess;
+  k_lineage_import<<<dim3((len + P - 1) / P * P - t0, c->cfg.num_layers), 128, 0, st>>>(dev_state(c), req, beam,
+                                                                                       len, t0, (const uint4*)buf);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_share_prefix(Ctx* c, int req, int beam, int share, int m, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_share_prefix<<<1, 256, 0, st>>>(dev_state(c), req, beam, share, m);
   c->launches++;
   return cudaGetLastError();
 }

@@ -138,7 +138,48 @@ size_t lineage_bytes(const tts_config_t& g, int len) {
   return (size_t)2 * g.num_layers * len * g.num_kv_heads * g.head_dim * 2;
 }
 
+// Page origins (f4): who created a page, where -- equal on every rank holding
+// a copy, distinct for pages whose contents may differ.  A full page's tokens
+// are a function of its origin, so a destination already holding the pages
+// of a lineage's prefix (same origins) need not receive them again.
+//   full prompt page k:                     0xFFFF << 16 | k
+//   the partial prompt page of gid g:       1 << 62 | g << 16 | k
+//   a page opened by gid g's append at the decode call tau of the request:
+//                                           (tau + 1) << 32 | g << 16 | k
+//   a fresh copy of a partially filled page (fork CoW; the partial last page
+//   of an imported lineage) for child gid c:  1 << 61 | (tau + 1) << 32 | c << 16 | k
+uint64_t origin_prompt(int k) { return (0xFFFFull << 16) | (uint64_t)k; }
+uint64_t origin_prompt_partial(int g, int k) { return (1ull << 62) | ((uint64_t)g << 16) | (uint64_t)k; }
+uint64_t origin_open(uint32_t tau, int g, int k) {
+  return ((uint64_t)(tau + 1) << 32) | ((uint64_t)g << 16) | (uint64_t)k;
+}
+uint64_t origin_copy(uint32_t tau, int c, int k) {
+  return (1ull << 61) | ((uint64_t)(tau + 1) << 32) | ((uint64_t)c << 16) | (uint64_t)k;
+}
+
 }  // namespace
+
+namespace tts {
+// Called by every append of the context (api.cu) before its launch: record
+// the origins of the pages the call opens, for requests tracking them.
+void span_note_append(Ctx* c, int n_req, const int32_t* req_ids, const std::vector<AllocItem>& items) {
+  if (c->spans.empty()) return;
+  const tts_config_t& g = c->cfg;
+  for (const AllocItem& it : items) {
+    const int64_t row_all = it.entry / g.max_pages_per_beam;
+    const int pos = (int)(it.entry % g.max_pages_per_beam);
+    const int req = (int)(row_all / g.max_beams), b = (int)(row_all % g.max_beams);
+    auto sp = c->spans.find(req);
+    if (sp == c->spans.end() || !sp->second.dedup) continue;
+    Span& S = sp->second;
+    S.origin[(size_t)b * g.max_pages_per_beam + pos] = origin_open(S.tau, S.gids[b], pos);
+  }
+  for (int i = 0; i < n_req; ++i) {
+    auto sp = c->spans.find(req_ids[i]);
+    if (sp != c->spans.end()) ++sp->second.tau;
+  }
+}
+}  // namespace tts
 
 extern "C" {
 
@@ -219,7 +260,7 @@ tts_status_t tts_comm_destroy(tts_ctx_t c) {
   return TTS_OK;
 }
 
-tts_status_t tts_span_init(tts_ctx_t c, int32_t req, int32_t n_global, const int32_t* caps_h) {
+tts_status_t tts_span_init(tts_ctx_t c, int32_t req, int32_t n_global, const int32_t* caps_h, int32_t dedup) {
   if (!c || !caps_h || !c->comm) return c && !c->comm ? TTS_ERR_STATE : TTS_ERR_INVALID_ARG;
   const int G = c->comm->nranks, me = c->comm->rank;
   if (req < 0 || req >= c->cfg.max_requests || c->n_beams[req] <= 0) return TTS_ERR_STATE;
@@ -235,7 +276,30 @@ tts_status_t tts_span_init(tts_ctx_t c, int32_t req, int32_t n_global, const int
   s.caps.assign(caps_h, caps_h + G);
   const int start = std::accumulate(caps_h, caps_h + me, 0);
   for (int i = 0; i < caps_h[me]; ++i) s.gids.push_back(start + i);
+  s.dedup = dedup != 0;
+  if (s.dedup) {
+    // only prompt pages so far (the request was just installed)
+    const tts_config_t& g = c->cfg;
+    const int len = c->lens[(int64_t)req * g.max_beams];
+    const int P = g.page_size, npg = (len + P - 1) / P;
+    s.origin.assign((size_t)g.max_beams * g.max_pages_per_beam, 0);
+    for (int i = 0; i < caps_h[me]; ++i) {
+      if (c->lens[(int64_t)req * g.max_beams + i] != len) return TTS_ERR_STATE;  // decoded already
+      for (int k = 0; k < npg; ++k)
+        s.origin[(size_t)i * g.max_pages_per_beam + k] =
+            (k + 1) * P <= len ? origin_prompt(k) : origin_prompt_partial(start + i, k);
+    }
+  }
   c->spans[req] = s;
+  return TTS_OK;
+}
+
+tts_status_t tts_span_stats(tts_ctx_t c, int32_t req, int64_t* migrated_bytes_h, int64_t* deduped_bytes_h) {
+  if (!c || !migrated_bytes_h || !deduped_bytes_h) return TTS_ERR_INVALID_ARG;
+  auto it = c->spans.find(req);
+  if (it == c->spans.end()) return TTS_ERR_STATE;
+  *migrated_bytes_h = it->second.migrated_bytes;
+  *deduped_bytes_h = it->second.deduped_bytes;
   return TTS_OK;
 }
 
@@ -313,6 +377,31 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
     }
   for (int q = 0; q < N; ++q)
     if (old_rank[q] < 0) return TTS_ERR_STATE;
+  // ---- 1b. f4: every rank's page origins ([cap_max][max_pages] uint64 per rank)
+  const int maxP = g.max_pages_per_beam;
+  const size_t org_bytes = (size_t)cap_max * maxP * 8;
+  std::vector<uint64_t> org_all;
+  std::vector<const uint64_t*> org_of(N, nullptr);  // gid -> its origin row
+  if (sp.dedup) {
+    org_all.resize((size_t)G * cap_max * maxP);
+    std::vector<uint64_t> mine((size_t)cap_max * maxP, 0);
+    std::copy(sp.origin.begin(), sp.origin.begin() + (size_t)n_loc * maxP, mine.begin());
+    if (cm.is_nccl) {
+      if (cm.stage_bytes < org_bytes * (G + 1)) return TTS_ERR_CAPACITY;
+      TTS_CUDA(cudaMemcpyAsync(cm.stage, mine.data(), org_bytes, cudaMemcpyHostToDevice, st));
+      if (tts::nccl().allgather(cm.stage, cm.stage + org_bytes, org_bytes, tts::kNcclUint8, cm.nc, st) != 0)
+        return TTS_ERR_NCCL;
+      TTS_CUDA(cudaMemcpyAsync(org_all.data(), cm.stage + org_bytes, org_bytes * G, cudaMemcpyDeviceToHost, st));
+      TTS_CUDA(cudaStreamSynchronize(st));
+    } else if (cm.host.allgather(cm.host.user, mine.data(), org_all.data(), org_bytes) != 0) {
+      return TTS_ERR_NCCL;
+    }
+    for (int r = 0; r < G; ++r)
+      for (int i = 0; i < cap_max; ++i) {
+        const tts::BeamRec& x = recs[(size_t)r * cap_max + i];
+        if (x.gid >= 0) org_of[x.gid] = org_all.data() + ((size_t)r * cap_max + i) * maxP;
+      }
+  }
   // ---- 2. global selection (the single-GPU kernel over gid-indexed scores)
   int32_t* dparent = c->ws_parent_all;
   TTS_CUDA(tts::launch_select_global(c, scores_all, N, M, dparent, st));
@@ -337,10 +426,35 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
   struct Xfer {
     int32_t p, src, dst;
     size_t bytes;
+    int32_t m, share;  // f4: leading pages the destination holds already (its beam `share`, gid)
+  };
+  const int P = g.page_size;
+  // f4: the longest run of leading FULL pages of p (same origins) that a beam
+  // of the destination holds; ties to the lowest gid
+  auto dedup_of = [&](int p, int dst, int& share) {
+    share = -1;
+    if (!sp.dedup) return 0;
+    int best = 0;
+    for (int y = 0; y < N; ++y) {
+      if (old_rank[y] != dst) continue;
+      const int full = std::min(len_of[p], len_of[y]) / P;
+      int k = 0;
+      while (k < full && org_of[p][k] == org_of[y][k]) ++k;
+      if (k > best) best = k, share = y;
+    }
+    return best;
   };
   std::vector<Xfer> xf;
   for (int r = 0; r < G; ++r)
-    for (int p : imports[r]) xf.push_back({p, old_rank[p], r, lineage_bytes(g, len_of[p])});
+    for (int p : imports[r]) {
+      int share;
+      const int m = dedup_of(p, r, share);
+      xf.push_back({p, old_rank[p], r, lineage_bytes(g, len_of[p] - m * P), m, share});
+      if (old_rank[p] == me) {
+        sp.migrated_bytes += (int64_t)lineage_bytes(g, len_of[p] - m * P);
+        sp.deduped_bytes += (int64_t)lineage_bytes(g, m * P);
+      }
+    }
   std::sort(xf.begin(), xf.end(), [](const Xfer& a, const Xfer& b) {
     return a.p != b.p ? a.p < b.p : a.dst < b.dst;
   });
@@ -364,7 +478,7 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
     // this rank's part of the round
     std::vector<int32_t> sdst, ssrc;
     std::vector<size_t> sbytes, rbytes, soff, roff;
-    std::vector<int32_t> rgid;
+    std::vector<int32_t> rgid, rm, rshare;
     size_t so = 0, ro = 0;
     for (size_t k = k0; k < k1; ++k) {
       const Xfer& x = xf[k];
@@ -380,6 +494,8 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
         rbytes.push_back(x.bytes);
         roff.push_back(ro);
         rgid.push_back(x.p);
+        rm.push_back(x.m);
+        rshare.push_back(x.share);
         ro += b;
       }
     }
@@ -393,12 +509,12 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
         if (x.src != me) continue;
         const int row = row_of.at(x.p);
         if (cm.is_nccl) {
-          TTS_CUDA(tts::launch_lineage_export(c, req, row, len_of[x.p], sbase + soff[i], st));
+          TTS_CUDA(tts::launch_lineage_export(c, req, row, len_of[x.p], sbase + soff[i], st, x.m * P));
         } else {
           // host transport: export into a device bounce buffer, then D2H
           void* dtmp = nullptr;
           TTS_CUDA(cudaMallocAsync(&dtmp, x.bytes, st));
-          TTS_CUDA(tts::launch_lineage_export(c, req, row, len_of[x.p], dtmp, st));
+          TTS_CUDA(tts::launch_lineage_export(c, req, row, len_of[x.p], dtmp, st, x.m * P));
           TTS_CUDA(cudaMemcpyAsync(sbase + soff[i], dtmp, x.bytes, cudaMemcpyDeviceToHost, st));
           TTS_CUDA(cudaFreeAsync(dtmp, st));
         }
@@ -434,10 +550,21 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
         TTS_CUDA(cudaMemcpyAsync(dtmp, src, rbytes[i], cudaMemcpyHostToDevice, st));
         src = dtmp;
       }
-      tts_status_t s = tts_lineage_import(c, req, row, len_of[p], src, stream);
-      if (s != TTS_OK) return s;
+      // the shared prefix from the local beam holding it, fresh pages for the
+      // rest (lowest free ids), the received tokens into them
+      const int m = rm[i], npg = (len_of[p] + P - 1) / P;
+      if (row >= g.max_beams) return TTS_ERR_CAPACITY;
+      if (m > 0) TTS_CUDA(tts::launch_share_prefix(c, req, row, row_of.at(rshare[i]), m, st));
+      std::vector<tts::AllocItem> items;
+      for (int k = m; k < npg; ++k)
+        items.push_back({((int64_t)req * g.max_beams + row) * g.max_pages_per_beam + k, 0, 0});
+      TTS_CUDA(tts::launch_alloc_host(c, items.data(), (int)items.size(), st));
+      TTS_CUDA(tts::launch_lineage_import(c, req, row, len_of[p], src, st, m * P));
+      c->lens[(int64_t)req * g.max_beams + row] = len_of[p];
+      c->n_rows[req] = std::max(c->n_rows[req], row + 1);
       if (dtmp) TTS_CUDA(cudaFreeAsync(dtmp, st));
       spare_of[p] = row;
+      if (sp.dedup) std::copy(org_of[p], org_of[p] + maxP, sp.origin.begin() + (size_t)row * maxP);
     }
     // the staging halves are reused by the next round
     TTS_CUDA(cudaStreamSynchronize(st));
@@ -451,6 +578,22 @@ tts_status_t tts_beam_select_fork_global(tts_ctx_t c, int32_t req, const float* 
   }
   tts_status_t s = tts_beam_fork_map(c, req, (int32_t)prow.size(), prow.data(), stream);
   if (s != TTS_OK) return s;
+  if (sp.dedup) {
+    // children take their parent row's origins; a partially filled last page
+    // that is a fresh copy -- every child but the first of its row (fork
+    // CoW), and the first child of an imported row (its page is a copy of
+    // the exporter's) -- gets a fresh origin
+    std::vector<uint64_t> old = sp.origin;
+    std::vector<char> seen((size_t)g.max_beams, 0);
+    for (size_t i = 0; i < prow.size(); ++i) {
+      const int pr = prow[i], len = c->lens[(int64_t)req * g.max_beams + (int)i];
+      std::copy(old.begin() + (size_t)pr * maxP, old.begin() + (size_t)(pr + 1) * maxP,
+                sp.origin.begin() + i * maxP);
+      if (len % P && (seen[pr] || pr >= n_loc))
+        sp.origin[i * maxP + (len - 1) / P] = origin_copy(sp.tau, children[me][i], (len - 1) / P);
+      seen[pr] = 1;
+    }
+  }
   sp.gids = children[me];
   if (child_rank_out) {
     void* d = tts::upload(c, child_rank.data(), (size_t)N * 4, st, &e);

@@ -54,6 +54,13 @@ struct Span {
   int n_global = 0;
   std::vector<int32_t> caps;
   std::vector<int32_t> gids;
+  // f4 (cross-GPU page deduplication): the origin of every page of every row
+  // ([max_beams][max_pages_per_beam]): who created the page where, identical
+  // on every rank holding a copy; a full page's content is a function of it
+  bool dedup = false;
+  std::vector<uint64_t> origin;
+  uint32_t tau = 0;  // decode calls of the request so far (the same on every rank)
+  int64_t migrated_bytes = 0, deduped_bytes = 0;
 };
 
 struct Ctx {
@@ -150,6 +157,8 @@ void upload2(Ctx* c, const void* a, size_t na, const void* b, size_t nb, cudaStr
              void** da, void** db);
 
 size_t workspace_bytes(const tts_config_t& cfg);
+// span.cu: page origins of the pages an append opens (f4)
+void span_note_append(Ctx* c, int n_req, const int32_t* req_ids, const std::vector<AllocItem>& items);
 
 // kernels (block_table.cu)
 cudaError_t launch_init_state(Ctx* c, cudaStream_t s);
@@ -170,8 +179,10 @@ cudaError_t launch_fork_tables(Ctx* c, const int32_t* reqs_d, int n_req, int n_o
                                const int32_t* new_lens_d = nullptr);
 cudaError_t launch_branch_rows(Ctx* c, int req, const int32_t* src_d, const int32_t* dst_d, int n, cudaStream_t s);
 cudaError_t launch_zero_tail(Ctx* c, const int32_t* items_d, int n, cudaStream_t s);  // (req, row, pos, ntok)
-cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t s);
-cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t s);
+// lineage copies of tokens [t0, len) (t0 a multiple of P; the buffer holds those tokens only)
+cudaError_t launch_lineage_export(Ctx* c, int req, int beam, int len, void* buf, cudaStream_t s, int t0 = 0);
+cudaError_t launch_lineage_import(Ctx* c, int req, int beam, int len, const void* buf, cudaStream_t s, int t0 = 0);
+cudaError_t launch_share_prefix(Ctx* c, int req, int beam, int share, int m, cudaStream_t s);
 cudaError_t launch_select_global(Ctx* c, const float* scores_all, int N, int M, int32_t* parent_out,
                                  cudaStream_t s);
 cudaError_t launch_release(Ctx* c, int req, int n_beams, cudaStream_t s);

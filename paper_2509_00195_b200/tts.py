@@ -99,7 +99,8 @@ def load() -> ctypes.CDLL:
             "tts_comm_init": [_P, _P, _I, _I, _P, ctypes.c_size_t],
             "tts_comm_init_host": [_P, _I, _I, ctypes.POINTER(tts_host_transport_t), ctypes.c_size_t],
             "tts_comm_destroy": [_P],
-            "tts_span_init": [_P, _I, _I, _P],
+            "tts_span_init": [_P, _I, _I, _P, _I],
+            "tts_span_stats": [_P, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)],
             "tts_span_gids": [_P, _I, _P],
             "tts_beam_select_fork_global": [_P, _I, _P, _I, _P, _P, _P],
             "tts_span_placement": [_I, _P, _P, _I, _P, _P],
@@ -420,8 +421,14 @@ class Context:
     def tts_comm_destroy(self):
         _check(self.lib.tts_comm_destroy(self.h), "tts_comm_destroy")
 
-    def tts_span_init(self, req: int, n_global: int, caps: Sequence[int]):
-        _check(self.lib.tts_span_init(self.h, req, n_global, _i32_host(caps)), "tts_span_init")
+    def tts_span_init(self, req: int, n_global: int, caps: Sequence[int], dedup: bool = False):
+        _check(self.lib.tts_span_init(self.h, req, n_global, _i32_host(caps), int(bool(dedup))), "tts_span_init")
+
+    def tts_span_stats(self, req: int):
+        """-> (bytes this rank sent for migrations, bytes deduplication saved it)."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(self.lib.tts_span_stats(self.h, req, ctypes.byref(a), ctypes.byref(b)), "tts_span_stats")
+        return a.value, b.value
 
     def tts_span_gids(self, req: int) -> list:
         n = int(self.n_beams(req))

@@ -66,7 +66,7 @@ def _compare_rank(ctx, rec, r, P, gids_model, where):
     assert snap["free"].tolist() == rec.free[r], f"{where}: free set"
 
 
-def _span_run(cfg, caps, transports, sample_every=7, pages=None):
+def _span_run(cfg, caps, transports, sample_every=7, pages=None, dedup=False):
     """Drive one spanning request through G contexts (rank r uses transports[r],
     or NCCL when transports is the string "nccl1"); compare with the models."""
     from paper_2509_00195_b200 import build
@@ -88,7 +88,7 @@ def _span_run(cfg, caps, transports, sample_every=7, pages=None):
             c.tts_comm_init(comm_unique_id(), 1, 0, stage)
         else:
             c.tts_comm_init_host(G, r, transports[r], stage_bytes=256 << 20)
-        c.tts_span_init(0, cfg.N, caps)
+        c.tts_span_init(0, cfg.N, caps, dedup)
 
     def sample(it):
         if it.t % sample_every:
@@ -97,7 +97,7 @@ def _span_run(cfg, caps, transports, sample_every=7, pages=None):
 
     orc = OracleRun(cfg, num_pages=pages * G)
     tr = orc.run(sample=sample)
-    model = SpanModel(N=cfg.N, caps=caps, num_pages=pages, P=cfg.P, prompt_len=cfg.prompt)
+    model = SpanModel(N=cfg.N, caps=caps, num_pages=pages, P=cfg.P, prompt_len=cfg.prompt, dedup=dedup)
     scale = 1.0 / math.sqrt(cfg.d)
     got, n_fork = {}, 0
     for it in workload.schedule(cfg, [0]):
@@ -145,6 +145,11 @@ def _span_run(cfg, caps, transports, sample_every=7, pages=None):
     for key, ref in tr.outputs.items():
         e = float((np.abs(got[key] - ref).max(-1) / np.abs(ref).max(-1)).max())
         assert e <= TOL, (key, e)
+    # migration traffic: what every rank sent (and saved) equals the model's tokens x bytes per token
+    tok_bytes = 2 * cfg.L * cfg.Hkv * cfg.d * 2
+    sent = [c.tts_span_stats(0) for c in ctxs]
+    assert sum(x[0] for x in sent) == model.migrated_tokens * tok_bytes
+    assert sum(x[1] for x in sent) == model.deduped_tokens * tok_bytes
     for c in ctxs:
         c.tts_comm_destroy()
     return n_fork
@@ -157,6 +162,18 @@ def test_thread_ranks_straggler_steps(G, caps):
                           n_steps=4, step_len=0, ln_mu=math.log(12), ln_sigma=1.0, ln_cap=40, seed=5150 + G)
     grp = ThreadGroup(G)
     assert _span_run(cfg, caps, [grp.transport(r) for r in range(G)]) == 3
+
+
+@pytest.mark.parametrize("G,caps", [(2, [8, 8]), (4, [4, 4, 4, 4])])
+def test_thread_ranks_dedup(G, caps):
+    """f4: migrated lineages reuse the leading pages the destination holds
+    (page origins); per-rank tables / refcounts / free sets bit-exact against
+    the deduplicating rank model, fewer bytes migrated, same outputs."""
+    from paper_2509_00195_b200.dist import ThreadGroup
+    cfg = workload.Config("span-dedup", R=1, N=sum(caps), M=4, L=2, Hq=28, Hkv=4, d=128, P=16, prompt=37,
+                          n_steps=4, step_len=0, ln_mu=math.log(40), ln_sigma=0.7, ln_cap=100, seed=6160 + G)
+    grp = ThreadGroup(G)
+    assert _span_run(cfg, caps, [grp.transport(r) for r in range(G)], dedup=True) == 3
 
 
 def test_thread_ranks_c5_shape():
@@ -193,7 +210,7 @@ def _gloo_worker(rank, world, port, queue):
         kp, vp = inp.prompt_kv(0)
         ctx.tts_block_table_init_request(0, caps[rank], cfg.prompt, kp, vp)
         ctx.tts_comm_init_host(world, rank, GlooTransport(), stage_bytes=64 << 20)
-        ctx.tts_span_init(0, cfg.N, caps)
+        ctx.tts_span_init(0, cfg.N, caps, True)
         scale = 1.0 / math.sqrt(cfg.d)
         snaps = []
         for it in workload.schedule(cfg, [0]):
@@ -235,7 +252,7 @@ def test_gloo_two_processes_share_cuda0():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    model = SpanModel(N=cfg.N, caps=caps, num_pages=400, P=cfg.P, prompt_len=cfg.prompt)
+    model = SpanModel(N=cfg.N, caps=caps, num_pages=400, P=cfg.P, prompt_len=cfg.prompt, dedup=True)
     k = 0
     for it in workload.schedule(cfg, [0]):
         model.append(it.active[0].tolist(), [("d", 0, it.t, g) for g in range(cfg.N)])

@@ -127,3 +127,53 @@ def test_span_model_matches_single_rank_oracle(seed):
             assert rec.free[r] == [p for p in range(4000) if cnt[p] == 0]
         # a rank's beams are in ascending gid, so every subtree's beams on a rank are adjacent rows
         assert all(gs == sorted(gs) for gs in m.gids)
+
+
+def test_dedup_hand_example():
+    """f4: N = 4, M = 2, ranks [2, 2], a 32-token prompt and a 16-token step,
+    then a second step.  Fork 1 keeps gids {0, 1} (both on rank 0): rank 1
+    imports gid 1's 48-token lineage; its beams share only the prompt with it
+    (2 full pages), so the import reuses rank 1's own prompt pages 0, 1 and
+    allocates one page for the step's tokens -- 16 tokens cross, not 48."""
+    m = SpanModel(N=4, caps=[2, 2], num_pages=16, P=16, prompt_len=32, dedup=True)
+    for t in range(16):
+        m.append([1, 1, 1, 1], [("d", 0, t, g) for g in range(4)])
+    rec = m.fork([0.9, 0.8, 0.1, 0.2], 2)
+    assert rec.tables[1] == [[0, 1, 4], [0, 1, 4]]
+    assert m.migrated_tokens == 16 and m.deduped_tokens == 32
+    assert m.gather(2) == [("p", 0, i) for i in range(32)] + [("d", 0, t, 1) for t in range(16)]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_dedup_preserves_sequences_and_saves_bytes(seed):
+    """Deduplication changes page ids, never what any beam reads: every beam's
+    token sequence equals the non-dedup model's at every fork; no more
+    tokens cross than without it; refcounts = table counts."""
+    rnd = random.Random(300 + seed)
+    G = rnd.choice([2, 4])
+    caps = [rnd.choice([2, 4])] * G
+    N = sum(caps)
+    M = rnd.choice([m for m in (2, 4) if N % m == 0])
+    prompt = rnd.choice([16, 37, 64])
+    a = SpanModel(N=N, caps=caps, num_pages=4000, P=16, prompt_len=prompt, dedup=True)
+    b = SpanModel(N=N, caps=caps, num_pages=4000, P=16, prompt_len=prompt, dedup=False)
+    t = 0
+    for step in range(4):
+        for _ in range(rnd.randint(8, 40)):
+            act = [rnd.random() < 0.9 for _ in range(N)]
+            for mm in (a, b):
+                mm.append(act, [("d", 0, t, g) for g in range(N)])
+            t += 1
+        sc = [rnd.randint(0, 3) / 3 for _ in range(N)]
+        ra, rb = a.fork(sc, M), b.fork(sc, M)
+        assert ra.parent_gid == rb.parent_gid and ra.child_rank == rb.child_rank
+        for g in range(N):
+            assert a.gather(g) == b.gather(g)
+        for r in range(G):
+            cnt = np.zeros(4000, dtype=int)
+            for row in ra.tables[r]:
+                for p in row:
+                    cnt[p] += 1
+            assert cnt.tolist() == ra.ref[r]
+    assert a.migrated_tokens <= b.migrated_tokens
+    assert a.migrated_tokens + a.deduped_tokens == b.migrated_tokens
