@@ -46,6 +46,7 @@ from synth import workload  # noqa: E402
 METRIC = "beam-steps/s and HBM GB/s (unique KV) vs roofline at 1/2/4/8 B200"
 UNIT = "beam-steps/s"
 DEFAULT_ROTATE = {"C1": 64, "C2": 32, "C3": 1, "C4": 1, "C5": 1}
+DEFAULT_PER_CALL = {"C1": 1, "C2": 4, "C3": 1, "C4": 1, "C5": 1}  # measured: C2 1 -> 0.50, 2 -> 0.59, 4 -> 0.69, 8 -> 0.70, 16 -> 0.68 of the copy peak
 HBM_SPEC_GBS = 8000.0  # north_star "~8 TB/s"
 
 
@@ -58,6 +59,8 @@ def parse():
     ap.add_argument("--config", default=None, choices=list(workload.CONFIGS),
                     help="default: C3 at N = 1, C4 at N > 1")
     ap.add_argument("--rotate", type=int, default=0)
+    ap.add_argument("--per-call", type=int, default=0,
+                    help="requests of the rotation per decode call (fixed-step configs; default per config)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=18.0)
@@ -228,7 +231,7 @@ class IOPipe:
 class Bench:
     """Drives one rank's requests through libtts with minimal host overhead."""
 
-    def __init__(self, cfg, greqs, dev_index, ring=8, pages_per_request=0):
+    def __init__(self, cfg, greqs, dev_index, ring=8, pages_per_request=0, per_call=1):
         from paper_2509_00195_b200 import build
         build.build()
         from paper_2509_00195_b200.runner import tts_config, Inputs
@@ -244,7 +247,10 @@ class Bench:
         self.inp = Inputs(cfg, self.dev)
         self.scale = ctypes.c_float(1.0 / math.sqrt(cfg.d))
         self.batched = cfg.step_len == 0  # straggler configs: one call per iteration for all requests
-        per_call = self.n if self.batched else 1
+        # fixed-step configs: `per_call` consecutive requests of the rotation per
+        # decode call (the C-ABI's n_req; 1 = one request per call)
+        per_call = self.n if self.batched else max(1, min(per_call, self.n))
+        self.per_call = per_call
         self.ring = []
         for i in range(ring):
             q, k, v = self.inp.step(10_000 + i, self.greqs[:per_call])
@@ -258,11 +264,14 @@ class Bench:
                 self.scores[(r, s)] = self.inp.scores(r, s).contiguous()
         self.local = {r: i for i, r in enumerate(self.greqs)}
         self.req_arr = {i: (ctypes.c_int32 * 1)(i) for i in range(self.n)}
+        # request chunks of a decode call (fixed-step configs: every request is live at every iteration)
+        self.chunks = [[self.local[r] for r in self.greqs[i:i + per_call]] for i in range(0, self.n, per_call)]
+        self.chunk_arr = [(ctypes.c_int32 * len(ch))(*ch) for ch in self.chunks]
         self.parent = torch.empty(self.n, cfg.N, dtype=torch.int32, device=self.dev)
         self.beam_steps = sum(int(a.sum()) for it in self.sched for a in it.active)
         self.stream = self.ctx.stream
         self.ncall = 0
-        self.n_calls = sum(1 if self.batched else len(it.reqs) for it in self.sched)
+        self.n_calls = sum(1 if self.batched else -(-len(it.reqs) // per_call) for it in self.sched)
         torch.cuda.synchronize(self.dev)
 
     def _chk(self, code, what):
@@ -298,8 +307,8 @@ class Bench:
             if e2e is None and not self.batched and stats_accum is None:
                 # hot loop: one C-ABI call per request and position, arguments pre-marshalled
                 qp, kp, vp = ptrs[it.t % nr]
-                for r in it.reqs:
-                    rc = decode(h, 1, self.req_arr[self.local[r]], None, kp, vp, qp, self.scale, outp, st)
+                for ch, arr in zip(self.chunks, self.chunk_arr):
+                    rc = decode(h, len(ch), arr, None, kp, vp, qp, self.scale, outp, st)
                     if rc:
                         self._chk(rc, "decode_step")
             else:
@@ -321,17 +330,16 @@ class Bench:
                                                             stats_accum[self.ncall].data_ptr(), st), "stats")
                         self.ncall += 1
                 else:
-                    for ri, r in enumerate(it.reqs):
+                    for ch, arr in zip(self.chunks, self.chunk_arr):
                         if e2e is not None:  # every call's q/k/v come from the host, its output goes back
                             q, k, v, out = e2e["pipe"].stage(hq, hk, hv)
-                        arr = self.req_arr[self.local[r]]
-                        self._chk(lib.tts_decode_step(h, 1, arr, None, k.data_ptr(), v.data_ptr(), q.data_ptr(),
-                                                      self.scale, out.data_ptr(), st), "decode_step")
+                        self._chk(lib.tts_decode_step(h, len(ch), arr, None, k.data_ptr(), v.data_ptr(),
+                                                      q.data_ptr(), self.scale, out.data_ptr(), st), "decode_step")
                         if e2e is not None:
                             e2e["pipe"].release()
                         if stats_accum is not None:
-                            self._chk(lib.tts_block_table_stats(h, 1, arr, None, stats_accum[self.ncall].data_ptr(),
-                                                                st), "stats")
+                            self._chk(lib.tts_block_table_stats(h, len(ch), arr, None,
+                                                                stats_accum[self.ncall].data_ptr(), st), "stats")
                             self.ncall += 1
             if it.forks or (seg is not None and it is self.sched[-1]):
                 if seg is not None:
@@ -700,7 +708,7 @@ def main():
         greqs = [rank * rot + i for i in range(rot)]
         scaling = "weak"
     if not span:
-        b = Bench(cfg, greqs, local, pages_per_request=ppr)
+        b = Bench(cfg, greqs, local, pages_per_request=ppr, per_call=args.per_call or DEFAULT_PER_CALL[cname])
     st = torch.cuda.current_stream(dev)
 
     # read-only HBM stream peak of this device (the attention
@@ -851,8 +859,8 @@ def main():
                        "prompt": cfg.prompt, "steps_x_len": f"{cfg.n_steps}x{cfg.step_len or 'lognormal'}",
                        "beam_steps_per_rank_step": b.beam_steps,
                        "l2": (f"unique KV per call {unique_b / max(1, b.n_calls) / 1e6:.0f} MB vs 126 MB L2; "
-                              + (f"rotation over {len(greqs)} independent requests, one per call" if not b.batched
-                                 else "batched requests")),
+                              + (f"rotation over {len(greqs)} independent requests, {b.per_call} per call"
+                                 if not b.batched else "batched requests")),
                        "parallelism": (f"beam-sharded x{ws} (one request's beams span the ranks; NCCL all-gather "
                                        "of scores + lineage migration per step)" if span else
                                        f"dp{ws} (independent requests per rank, no data-path collective)")},
