@@ -127,7 +127,7 @@ tts_status_t tts_device_status(tts_ctx_t ctx, void* stream, tts_status_t* out_h)
 int64_t tts_launch_count(tts_ctx_t ctx);
 
 /* Name of the attention kernel this context's decode calls launch:
- * "k_tree_umma" (tcgen05, d = 128, 4 <= G <= 16, two CTAs resident per SM) or
+ * "k_tree_umma" (tcgen05, d = 128, 4 <= G <= 16, one CTA resident per SM) or
  * "k_tree_attn" (mma.sync: d = 64, G < 4, or a device where the tcgen05
  * kernel's residency does not hold). */
 const char* tts_attention_kernel(tts_ctx_t ctx);

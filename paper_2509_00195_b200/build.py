@@ -32,7 +32,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    extra = os.environ.get("NVCC_EXTRA", "").split()  # tools: A/B variants (e.g. -DTTS_WAIT_NOHINT)
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", *extra,
            "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
            "-o", LIB + ".tmp", *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)

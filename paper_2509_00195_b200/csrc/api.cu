@@ -416,7 +416,7 @@ static tts_status_t attn_prepare(tts_ctx_t c, int32_t layer_begin, int32_t layer
   if (ap.umma) {
     // 128-row tiles: balanced runs of <= umma_max_beams beams of one request.
     // The largest groups (a page shared inside a group is staged once) that
-    // still give >= 3/4 of a round of tiles for the 2 CTAs per SM of the
+    // still give >= 3/4 of a round of tiles for the one CTA per SM of the
     // persistent kernel; a smaller remainder is split over all CTAs there
     // (stream-K).  Measured (C2, one request per call): 4-beam groups, 224
     // whole tiles, 40 us per call vs 16-beam groups, 56 tiles split ~5 ways,
@@ -424,7 +424,7 @@ static tts_status_t attn_prepare(tts_ctx_t c, int32_t layer_begin, int32_t layer
     // of a tile keeps all four softmax warps busy, a private tail one).
     int maxb = tts::umma_max_beams(c);
     if (c->env_group_beams) maxb = std::max(1, std::min(maxb, c->env_group_beams));
-    const int64_t want = (3ll * 2 * c->num_sms + 3) / 4;
+    const int64_t want = (3ll * c->num_sms + 3) / 4;
     auto group_size = [&](int cap) {
       int gb = 1;
       for (int i = 0; i < n_req; ++i) {

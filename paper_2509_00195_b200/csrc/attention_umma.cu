@@ -12,20 +12,25 @@
 //             adjacent (ledger C5) -- the ordered list of its
 //             DISTINCT pages, each with its member-beam bitmask and valid-token
 //             count.
-// k_tree_umma a4 (+ a5): persistent, 2 CTAs per SM.  A tile is (group, kv
-//             head, layer): the group's beams x the G query heads of the kv
-//             head, <= 128 rows, against the group's page list.  Whole tiles
-//             round-robin first, then the rest split over all CTAs (stream-K)
-//             and merged through a global partial buffer.
-// Per unit of two pages:
-//   producer warp   TMA (16x128 bf16 K / fp16 V tiles, SWIZZLE_128B) -> smem ring
-//   S warp          S[128 x 32] = Q . K^T     tcgen05.mma kind::f16, S in TMEM
-//   softmax warps   one thread per row: tcgen05.ld S; mask rows whose beam does not
-//                   reference the page and token slots >= ntok; fp32 online softmax
-//                   with lazy rescale (O rescaled in TMEM only when the running max
-//                   grows by > 2^8); P in fp16 -> tcgen05.st over S
-//   PV warp         O[128 x 128] += P . V   fp16 x fp16 (A from TMEM; V is kept in
-//                   fp16 in the pool, MN-major operand; ledger C14)
+// k_tree_umma a4 (+ a5): persistent, one CTA per SM (512 TMEM columns).  A
+//             tile is (group, kv head, layer): the group's beams x the G query
+//             heads of the kv head, <= 128 rows, against the group's page list.
+//             Whole tiles round-robin first, then the rest split over all CTAs
+//             (stream-K) and merged through a global partial buffer.
+// Per unit of eight pages (128 tokens, 64 KiB of K + V):
+//   K producer warp   TMA (two 16 x 64 bf16 half tiles per page, SWIZZLE_128B) -> K ring (3 units)
+//   V producer warp   TMA (one 16 x 128 fp16 tile per page) -> V ring (3 units)
+//   S warp            S[128 x 128] = Q . K^T   8 x tcgen05.mma kind::f16 (Q in smem), S in TMEM
+//   softmax warps     8 warps, two per TMEM lane quadrant (one row per thread), each
+//                     the S columns of four pages: tcgen05.ld S; mask rows whose beam
+//                     does not reference the page and token slots >= ntok; fp32
+//                     online softmax with lazy rescale (O rescaled in TMEM only when
+//                     the running max grows by > 2^8; the two halves of a row
+//                     exchange their maxima through shared memory); P in fp16 ->
+//                     tcgen05.st over S
+//   PV warp           O[128 x 128] += P . V   fp16 x fp16 (A from TMEM; V is kept in
+//                     fp16 in the pool, MN-major operand; ledger C14)
+// Three S/P buffers in TMEM keep three units between S = Q K^T and O += P V.
 // Each distinct page is fetched once per tile and multiplied against all its
 // rows: every GQA head and every beam of the tile that references it.
 #include <cstdlib>
@@ -41,32 +46,47 @@ using namespace sm100;
 constexpr int kP = 16;
 constexpr int kD = 128;
 constexpr int kRows = 128;
-constexpr int kU = 2;                        // pages per unit
-constexpr int kNS = 6;                       // ring slots (units)
+constexpr int kU = 8;                        // pages per unit (128 tokens: S is 128 x 128)
 constexpr int kTile = kP * kD * 2;           // 4 KiB: one (page, kv head) K or V tile
-constexpr int kSlot = 2 * kU * kTile;        // 16 KiB: K tiles then V tiles
-constexpr int kRing = kNS * kSlot;           // 64 KiB
-constexpr int kThreads = 224;                // warps 0-3 softmax, 4 producer, 5 S issuer, 6 PV issuer
-constexpr int kTmemCols = 256;               // O [0,128), Q [128,192), S/P [192,224), [224,256)
-constexpr int kSCols = kU * kP;              // 32
+constexpr int kKSlot = kU * kTile;           // 32 KiB: K of a unit, [d half][page][16 tokens][128 B]
+constexpr int kVSlot = kU * kTile;           // 32 KiB: V of a unit, [page][d half][16 tokens][128 B]
+constexpr int kNK = 3;                       // K ring slots (released when S = Q K^T has completed)
+constexpr int kNV = 3;                       // V ring slots (released when O += P V has completed)
+constexpr int kNM = 6;                       // unit metadata ring (>= kNK + kNSB: see the K producer)
+constexpr int kUH = kU / 2;                  // pages per softmax warp half
+constexpr int kThreads = 384;                // warps 0-7 softmax, 8 K producer, 9 V producer, 10 S issuer, 11 PV issuer
+constexpr int kSoftmaxWarps = 8;
+constexpr int kTmemCols = 512;               // O [0,128), S/P buffers [128,256), [256,384), [384,512)
+constexpr int kNSB = 3;                      // S buffers (P overwrites S; a buffer is free once PV has read P)
+constexpr int kSCols = kU * kP;              // 128
+constexpr int kTS = 128;                     // first S buffer column
 
 constexpr int kMaxGroups = 1024;             // beam groups per call (smem prefix of their unit counts)
-constexpr int kOffRing = 0;
-constexpr int kOffMeta = kOffRing + kRing;
-constexpr int kOffBar = kOffMeta + kNS * kU * 16;
-constexpr int kNumBars = 2 * kNS + 9;        // full, empty, sfull[2], pfull[2], pv[2], qready, ofree, qtaken
-constexpr int kOffScr = (kOffBar + kNumBars * 8 + 16 + 15) / 16 * 16;  // int4 scratch: 16-B aligned
-constexpr int kScrItems = 64;                // producer: one batch of 32 units (2 items each)
-constexpr int kOffPre = kOffScr + kScrItems * 16;
-constexpr int kOffInfo = kOffPre + (kMaxGroups + 1) * 4;
-constexpr int kSmemBytes = kOffInfo + 16 + 1024;
-static_assert(2 * (kSmemBytes + 1024) <= 228 * 1024, "two CTAs per SM");
-static_assert(3 * (kSmemBytes + 1024) > 228 * 1024, "at most two CTAs per SM (plan double-buffer argument)");
-static_assert(kOffScr % 16 == 0 && kOffMeta % 16 == 0 && kOffBar % 8 == 0, "shared-memory alignment");
+constexpr int kOffK = 0;
+constexpr int kOffV = kOffK + kNK * kKSlot;
+constexpr int kOffQ = kOffV + kNV * kVSlot;  // Q of the piece: [d half][128 rows][128 B], SWIZZLE_128B (A of S = Q K^T)
+constexpr int kOffMeta = kOffQ + kRows * kD * 2;
+constexpr int kOffBar = kOffMeta + kNM * kU * 16;
+// kfull[kNK], kempty[kNK], vfull[kNV], vempty[kNV], sfull[2], pfull[2], pv[2], qready, ofree, qtaken
+// kfull[kNK], kempty[kNK], vfull[kNV], vempty[kNV], sfull[kNSB], pfull[kNSB], pv[kNSB], qready, ofree, qtaken
+constexpr int kNumBars = 2 * kNK + 2 * kNV + 3 * kNSB + 3;
+constexpr int kOffXm = (kOffBar + kNumBars * 8 + 16 + 15) / 16 * 16;  // row max exchange [2 units][2 halves][128]
+constexpr int kOffInfo = kOffXm + 4 * kRows * 4;
+// The dynamic shared memory starts 1024-B aligned (the kernel has no static
+// shared memory; checked at run time): no alignment slack
+constexpr int kSmemBytes = kOffInfo + 16;
+// one CTA per SM (the 512 TMEM columns), and at most one: the plan
+// double-buffer argument (umma_prepare) needs the next call's CTAs to become
+// resident only after this call's have exited
+static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
+static_assert(2 * (kSmemBytes + 1024) > 228 * 1024, "at most one CTA per SM (plan double-buffer argument)");
+static_assert(kOffMeta % 16 == 0 && kOffBar % 8 == 0 && kOffXm % 16 == 0 && kOffQ % 1024 == 0, "shared-memory alignment");
+static_assert(kNM >= kNK + kNSB, "metadata ring reuse distance");
+static_assert(kOffV % 1024 == 0 && kKSlot % 1024 == 0, "SWIZZLE_128B atoms");
 
 #ifdef TTS_PROF
 // per CTA (last launch) x warp: accumulated cycles [0..5] + counters (tools/prof.py)
-__device__ long long g_prof[512][8][16];
+__device__ long long g_prof[512][12][16];
 #define PROF_DECL long long pf_[16] = {}; long long pf_t = clock64()
 #define PROF_MARK(k)                   \
   do {                                 \
@@ -91,6 +111,10 @@ __device__ long long g_prof[512][8][16];
 __device__ long long g_trace[1024][8];
 __device__ long long g_trace2[1024][8];
 __device__ long long g_cta[4096][4];  // per CTA of the last launch: globaltimer at start / loop end / exit, units | smid << 32
+// per call (launch id % 32768): [0] first attention CTA start, [1] last attention CTA exit,
+// [2] first k_plan block start, [3] last k_plan block exit (globaltimer; min/max by atomics)
+__device__ unsigned long long g_lspan[32768][4];
+#define TTS_SPAN(id, k, v, op) op(&g_lspan[(id) & 32767][(k)], (unsigned long long)(v))
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -115,6 +139,9 @@ __device__ __forceinline__ long long gtimer() {
 #define TTS_CTA(ev, v) \
   do {                 \
   } while (0)
+#define TTS_SPAN(id, k, v, op) \
+  do {                         \
+  } while (0)
 #define TTS_TR(j, ev) \
   do {                \
   } while (0)
@@ -133,11 +160,13 @@ struct UParams {
   int32_t* status;
   float* partial;             // [2 * gridDim.x][m 128 | l 128 | O 128 x 128]: split tiles' partial states
   int32_t* tile_cnt;          // [n_tiles] pieces of a split tile done (reset by its merger)
+  int* pre;                   // [gridDim.x][kMaxGroups + 1] per-CTA scratch: prefix of units per group
   int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
   int round_robin;            // beam b of a group -> lane quadrant b % 4 (else blocks of consecutive beams)
   int split_partial_round;    // a last partial round of tiles goes through stream-K (else whole if >= 3/4 full)
   int64_t num_pages;
   float scale_log2;
+  int launch_id;              // call counter (TTS_TRACE launch spans only)
 };
 constexpr int kPartFloats = 2 * kRows + kRows * kD;
 constexpr int kMaxCtas = 2 * 160;  // partial-state slots are sized for this many CTAs
@@ -174,12 +203,25 @@ struct PlanParams {
   int32_t* counts;
   int n_groups, layer_begin, n_call, Hkv, maxB, maxP;
   int64_t num_pages;
+  int launch_id;  // call counter (TTS_TRACE launch spans only)
 };
-constexpr int kPlanThreads = 128;  // small enough to co-reside with two attention CTAs per SM
+constexpr int kPlanThreads = 128;  // small enough to co-reside with the attention CTA of an SM
+// attention registers per thread: leaves 64 per thread of a k_plan block on the SM
+constexpr int kMaxRegs = (65536 - 64 * kPlanThreads) / kThreads / 8 * 8;
+static_assert(kMaxRegs >= 128, "register budget");
 
 __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __grid_constant__ UInline inl) {
   __shared__ int s_len[32];
   __shared__ int s_wsum[kPlanThreads / 32];
+#ifdef TTS_TRACE
+  if (threadIdx.x == 0) TTS_SPAN(p.launch_id, 2, gtimer(), atomicMin);
+  struct SpanEnd {
+    int id;
+    __device__ ~SpanEnd() {
+      if (threadIdx.x == 0) TTS_SPAN(id, 3, gtimer(), atomicMax);
+    }
+  } span_end_{p.launch_id};
+#endif
   // Programmatic dependent launch: this grid may run while the previous call's
   // attention kernel still streams its pages.  Nothing here conflicts with it:
   // the plan goes to the other half of the double-buffered items workspace,
@@ -326,8 +368,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 }
 
 // ---------------------------------------------------------------------------
-// Persistent attention (a4 + a5), 2 CTAs per SM.  The call's work is a
-// sequence of units (2 distinct pages of one tile), tiles ordered (layer, kv
+// Persistent attention (a4 + a5), one CTA per SM.  The call's work is a
+// sequence of units (8 distinct pages of one tile), tiles ordered (layer, kv
 // head, group) with the group fastest.  Whole tiles go round-robin while there
 // are at least 3/4 as many left as CTAs (phase 1); the units of the rest are
 // split evenly over the CTAs (phase 2, stream-K).  A CTA's phase-2 range covers whole
@@ -339,43 +381,54 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 // kPoly: exponentials on the FMA/ALU pipes (ex2_poly2) instead of MUFU: 1 = every other pair, 2 = all
 // instead of MUFU.
 template <int kPoly>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __maxnreg__(kMaxRegs)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = su32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* bp = smem_raw + (base - raw);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t base = su32(smem_raw);
+  uint8_t* bp = smem_raw;
+  if (base & 1023u) {  // (never seen: the layout has no slack for a misaligned base)
+    if (threadIdx.x == 0) atomicCAS(p.status, 0, (int32_t)TTS_ERR_UNSUPPORTED);
+    return;
+  }
   int4* meta = reinterpret_cast<int4*>(bp + kOffMeta);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bp + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
-  int* s_pre = reinterpret_cast<int*>(bp + kOffPre);  // [n_groups + 1] exclusive prefix of units per group
+  // [n_groups + 1] exclusive prefix of units per group: this CTA's slice of a
+  // global scratch (no room left in shared memory; read through L1)
+  int* s_pre = p.pre + (size_t)blockIdx.x * (kMaxGroups + 1);
   int* s_info = reinterpret_cast<int*>(bp + kOffInfo);  // [0] merger flag
-  const uint32_t b_full = su32(bars), b_empty = b_full + 8 * kNS, b_sfull = b_empty + 8 * kNS,
-                 b_pfull = b_sfull + 16, b_pv = b_pfull + 16, b_qready = b_pv + 16, b_ofree = b_qready + 8,
-                 b_qtaken = b_ofree + 8;
+  float* s_xm = reinterpret_cast<float*>(bp + kOffXm);
+  const uint32_t b_kfull = su32(bars), b_kempty = b_kfull + 8 * kNK, b_vfull = b_kempty + 8 * kNK,
+                 b_vempty = b_vfull + 8 * kNV, b_sfull = b_vempty + 8 * kNV, b_pfull = b_sfull + 8 * kNSB,
+                 b_pv = b_pfull + 8 * kNSB, b_qready = b_pv + 8 * kNSB, b_ofree = b_qready + 8, b_qtaken = b_ofree + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
   if (threadIdx.x == 0) TTS_CTA(0, gtimer());
+  if (threadIdx.x == 0) TTS_SPAN(p.launch_id, 0, gtimer(), atomicMin);
   // the next call's k_plan may start as soon as every CTA of this grid runs
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNS; ++i) {
-      bar_init(b_full + 8 * i, 1);
-      bar_init(b_empty + 8 * i, 1);
+    for (int i = 0; i < kNK; ++i) {
+      bar_init(b_kfull + 8 * i, 1);
+      bar_init(b_kempty + 8 * i, 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kNV; ++i) {
+      bar_init(b_vfull + 8 * i, 1);
+      bar_init(b_vempty + 8 * i, 1);
+    }
+    for (int i = 0; i < kNSB; ++i) {
       bar_init(b_sfull + 8 * i, 1);
-      bar_init(b_pfull + 8 * i, 4);
+      bar_init(b_pfull + 8 * i, kSoftmaxWarps);
       bar_init(b_pv + 8 * i, 1);
     }
-    bar_init(b_qready, 4);
-    bar_init(b_ofree, 4);
+    bar_init(b_qready, kSoftmaxWarps);
+    bar_init(b_ofree, kSoftmaxWarps);
     bar_init(b_qtaken, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == 10) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -384,19 +437,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem, t_q = tmem + 128, t_s = tmem + 192;
+  const uint32_t t_o = tmem, t_s = tmem + kTS;
+  const uint32_t s_q = base + kOffQ;
   const int G = p.G;
   const int ng = p.n_groups;
   const int T = p.n_layers * p.Hkv * ng;
   const int Cg = gridDim.x;
-  // whole-tile rounds (phase 1); a last round that would fill >= 3/4 of the
-  // CTAs is also taken whole (cheaper than splitting and merging every tile)
-  int k1 = T / Cg;
-  if (4 * (T - k1 * Cg) >= 3 * Cg && !p.split_partial_round) ++k1;
-  const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   auto group_of = [&](int gi) { return p.groups ? p.groups[gi] : inl.g[gi]; };
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-  const int r = threadIdx.x;
+  const int r = (warp & 3) * 32 + lane;  // softmax warps: the TMEM lane (tile row) of this thread
   // Rows of a tile, balanced over the four lane quadrants (softmax warps):
   // warp w holds beams [w*bpw, (w+1)*bpw) of the group, G consecutive lanes
   // per beam (host: bpw * G <= 32).  A page's exponentials are computed only
@@ -419,27 +468,25 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint4* src = reinterpret_cast<const uint4*>(
         p.q + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + (ok ? bl : 0)) * p.Hq + kh * G +
                (ok ? hd : 0)) * kD);
+    {
+      // warp half hf = warp >> 2 writes d columns [64 hf, 64 hf + 64) of row r:
+      // 16-B chunk c at (c ^ (r & 7)) within the row's 128 B (SWIZZLE_128B)
+      const int hf = warp >> 2;
+      uint4 v[8];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      uint32_t h[32];
+      for (int c = 0; c < 8; ++c) v[c] = ok ? __ldg(src + hf * 8 + c) : make_uint4(0, 0, 0, 0);
+      const uint32_t row = s_q + hf * (kRows * 128) + r * 128;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 v = ok ? __ldg(src + hf * 8 + c) : make_uint4(0, 0, 0, 0);
-        h[4 * c] = v.x;
-        h[4 * c + 1] = v.y;
-        h[4 * c + 2] = v.z;
-        h[4 * c + 3] = v.w;
-      }
-      tc_st32(t_q + lane_off + hf * 32, h);
+      for (int c = 0; c < 8; ++c)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((c ^ (r & 7)) << 4)), "r"(v[c].x),
+                     "r"(v[c].y), "r"(v[c].z), "r"(v[c].w)
+                     : "memory");
     }
-    tc_wait_st();
-    tc_fence_before();
+    // generic-proxy stores -> the tensor core's (async proxy) operand reads
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) bar_arrive(b_qready);
   };
-  // the first phase-1 tile (blockIdx.x) is known without the plan: its Q goes
-  // to TMEM while k_plan still runs (q is not written by k_plan)
-  if (warp < 4 && n1 > 0) load_q((int)blockIdx.x % ng, (int)blockIdx.x / ng);
   // Programmatic dependent launch: this grid starts while k_plan (the call's
   // append + plan) runs; everything below reads what k_plan writes.
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -450,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     int run = 0;
     for (int i0 = 0; i0 < p.n_groups; i0 += 32) {
       const int i = i0 + lane;
-      const int u = i < p.n_groups ? (__ldg(p.counts + i) + 1) / 2 : 0;
+      const int u = i < p.n_groups ? (__ldg(p.counts + i) + kU - 1) / kU : 0;
       int x = u;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -471,6 +518,19 @@ __global__ void __launch_bounds__(kThreads, 2)
   // from HBM about once (L2).  Phase 2: the units of the remaining tiles, split
   // over the CTAs (stream-K).
   auto F = [&](int t) { return (int64_t)(t / ng) * S + s_pre[t % ng]; };  // first unit of tile t
+  int maxu = 0;
+  for (int i = 0; i < ng; ++i) maxu = max(maxu, s_pre[i + 1] - s_pre[i]);
+  // Whole-tile rounds (phase 1): every full round but the last, unless the
+  // tiles end exactly on a round (or a last partial round fills >= 3/4 of the
+  // CTAs: taken whole too, cheaper than splitting and merging every tile).
+  // The rest goes through phase 2; if k1 rounds of the largest tile could
+  // exceed a CTA's fair share U / C, no phase 1 at all (an even split of
+  // every unit, always balanced).
+  int k1 = T / Cg;
+  if (4 * (T - k1 * Cg) >= 3 * Cg && !p.split_partial_round) ++k1;
+  else if (k1 > 0 && T > k1 * Cg) --k1;
+  if (k1 > 0 && T > k1 * Cg && (int64_t)k1 * maxu + 1 > U / Cg) k1 = 0;
+  const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   const int64_t base2 = F(min(k1 * Cg, T));
   const int64_t U2 = U - base2;
   // phase-2 CTAs: every one gets >= 1 unit (a split tile's pieces are then
@@ -479,9 +539,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // fair share U / C): CTA c's phase-2 range tops its phase-1 tiles up to
   // ~(c+1) U / C units in total, start2(c) = base2 + c U / C - (phase-1 units
   // of CTAs < c).  Otherwise an even split of the phase-2 units.
-  int maxu = 0;
-  for (int i = 0; i < ng; ++i) maxu = max(maxu, s_pre[i + 1] - s_pre[i]);
-  const bool bal = k1 > 0 && U2 > 0 && (int64_t)k1 * maxu + 1 <= U / Cg;
+  const bool bal = k1 > 0 && U2 > 0;
   const int C2 = bal ? Cg : (int)min((int64_t)Cg, U2);
   auto f1 = [&](int cc) {  // phase-1 units of CTAs [0, cc)
     int64_t a = 0;
@@ -533,15 +591,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     pslot = 2 * blockIdx.x + (u == ua2 ? 0 : 1);
   };
 
-  if (warp == 4) {
-    // ========================= producer: TMA =========================
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
-    }
+  if (warp == 8 || warp == 9) {
+    // ================= producers: TMA (warp 4: K + unit metadata, warp 5: V) =================
+    // Lane k < kU owns page k of a unit: it loads the plan item (one unit
+    // ahead) and issues that page's TMA; lane 0 arms the slot's barrier first.
+    const bool is_k = warp == 8;
+    if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(is_k ? &tmk : &tmv)) : "memory");
     // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
     PROF_DECL;
-    int slot = 0;
+    const int nslot = is_k ? kNK : kNV;
+    const uint32_t b_f = is_k ? b_kfull : b_vfull, b_e = is_k ? b_kempty : b_vempty;
+    int slot = 0, js = 0;
     uint32_t ph = 0;
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
@@ -551,72 +611,53 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int nit = __ldg(p.counts + gi);
       const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
       const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
-      // the whole warp runs the issue loop on warp-uniform values (the
-      // unit's pages are broadcast from the lane that loaded them); one
-      // elected lane writes the slot's metadata and issues the TMAs
-      auto issue = [&](const int4& m0, const int4& m1) {
-        PROF_MARK(1);
-        bar_wait(b_empty + 8 * slot, ph ^ 1u);
+      auto item = [&](int v) {
+        const int i = kU * v + lane;
+        return (lane < kU && v < j1 && i < nit) ? __ldg(its + i) : make_int4(-2, 0, 0, 0);
+      };
+      int4 nx = item(j0);
+      for (int v = j0; v < j1; ++v, ++js) {
+        const int4 m = nx;
+        nx = item(v + 1);
+        PROF_MARK(2);
+        bar_wait(b_e + 8 * slot, ph ^ 1u);
         PROF_MARK(0);
-        if (elect_one()) {
-          meta[slot * kU] = m0;
-          meta[slot * kU + 1] = m1;
-          const uint32_t fb = b_full + 8 * slot;
-          bar_expect(fb, (uint32_t)(((m0.x >= 0) + (m1.x >= 0)) * 2 * kTile));
-          const uint32_t sb = base + kOffRing + slot * kSlot;
-          // K: [d half][page][16 tokens][128 B] (one 32-row K-major operand for
-          // S = Q K^T over both pages); V: [page][d half][16][128 B] (3D box)
-          const int y0 = (int)((layer_rows + (int64_t)m0.x * p.Hkv + kh) * kP);
-          tma2d(sb, &tmk, 0, y0, fb);
-          tma2d(sb + 2 * kTile / 2, &tmk, 64, y0, fb);
-          tma3d(sb + kU * kTile, &tmv, 0, y0, 0, fb);
-          if (m1.x >= 0) {
-            const int y1 = (int)((layer_rows + (int64_t)m1.x * p.Hkv + kh) * kP);
-            tma2d(sb + kTile / 2, &tmk, 0, y1, fb);
-            tma2d(sb + 3 * kTile / 2, &tmk, 64, y1, fb);
-            tma3d(sb + (kU + 1) * kTile, &tmv, 0, y1, 0, fb);
+        if (lane == 0) TTS_TR2(js, is_k ? 3 : 4);
+        const bool has = m.x >= 0;
+        const uint32_t np = __popc(__ballot_sync(0xffffffffu, has));
+        const uint32_t fb = b_f + 8 * slot;
+        if (is_k && lane < kU) meta[(js % kNM) * kU + lane] = m;
+        if (lane == 0) bar_expect(fb, np * (uint32_t)kTile);
+        __syncwarp();
+        if (has) {
+          const int y = (int)((layer_rows + (int64_t)m.x * p.Hkv + kh) * kP);
+          if (is_k) {
+            // K: [d half][page][16 tokens][128 B] (one 128-row K-major operand over the unit)
+            const uint32_t sb = base + kOffK + slot * kKSlot + lane * (kTile / 2);
+            tma2d(sb, &tmk, 0, y, fb);
+            tma2d(sb + kU * (kTile / 2), &tmk, 64, y, fb);
+          } else {
+            // V: [page][d half][16][128 B] (3D box)
+            tma3d(base + kOffV + slot * kVSlot + lane * kTile, &tmv, 0, y, 0, fb);
           }
         }
         __syncwarp();
-        if (++slot == kNS) {
+        if (++slot == nslot) {
           slot = 0;
           ph ^= 1u;
-        }
-      };
-      // 32 units per batch (lane = unit); the next batch's loads are in
-      // flight while the current one is issued
-      int4 a0 = make_int4(-2, 0, 0, 0), a1 = a0;
-      auto load = [&](int v0) {
-        const int v = v0 + lane;
-        if (v < j1) {
-          a0 = __ldg(its + 2 * v);
-          a1 = 2 * v + 1 < nit ? __ldg(its + 2 * v + 1) : make_int4(-2, 0, 0, 0);
-        }
-      };
-      load(j0);
-      for (int v0 = j0; v0 < j1; v0 += 32) {
-        const int4 b0 = a0, b1 = a1;
-        if (v0 + 32 < j1) load(v0 + 32);
-        PROF_MARK(2);
-        const int n = min(32, j1 - v0);
-        for (int k = 0; k < n; ++k) {
-          const int4 m0 = make_int4(__shfl_sync(~0u, b0.x, k), __shfl_sync(~0u, b0.y, k), __shfl_sync(~0u, b0.z, k),
-                                    __shfl_sync(~0u, b0.w, k));
-          const int4 m1 = make_int4(__shfl_sync(~0u, b1.x, k), __shfl_sync(~0u, b1.y, k), __shfl_sync(~0u, b1.z, k),
-                                    __shfl_sync(~0u, b1.w, k));
-          issue(m0, m1);
         }
         PROF_MARK(1);
       }
     }
-    PROF_FLUSH(4);
-  } else if (warp == 5) {
+    PROF_FLUSH(warp);
+  } else if (warp == 10) {
     // ========================= S issuer: S = Q K^T =========================
     // The whole warp runs the loop so that descriptors stay warp-uniform; one
     // elected lane issues.  S and PV are issued by two warps so that neither
     // waits behind the other's issue (the tensor pipe runs both in issue order).
-    constexpr uint32_t id_s = idesc_bf16(kRows, kU * kP, false);
-    const uint64_t dk0 = sdesc(base + kOffRing, 16, 1024, 2);  // K tiles: K-major SW128
+    constexpr uint32_t id_s = idesc_bf16(kRows, kSCols, false);
+    const uint64_t dk0 = sdesc(base + kOffK, 16, 1024, 2);  // K tiles: K-major SW128
+    const uint64_t dq0 = sdesc(s_q, 16, 1024, 2);            // Q: K-major SW128
     // (TTS_PROF: [0] waiting for K, [1] waiting for the S buffer, [2] issuing, [3] waiting for Q)
     PROF_DECL;
     int js = 0;
@@ -630,36 +671,38 @@ __global__ void __launch_bounds__(kThreads, 2)
       // softmax warps load the next Q only after this wait (no parity aliasing)
       if (j1 == j0 && lane == 0) bar_arrive(b_qtaken);
       for (int j = j0; j < j1; ++j, ++js) {
-        const int slot = js % kNS;
-        if (lane == 0) TTS_TR(js, 0);
+        const int slot = js % kNK;
         PROF_MARK(2);
-        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        bar_wait(b_kfull + 8 * slot, (js / kNK) & 1u);
         PROF_MARK(0);
-        if (lane == 0) TTS_TR(js, 1);
-        // S buffer js & 1 holds P(js - 2) until PV(js - 2) has read it
-        if (js >= 2) bar_wait(b_pv + 8 * (js & 1), ((js - 2) >> 1) & 1u);
+        if (lane == 0) TTS_TR(js, 0);
+        // S buffer js % 3 holds P(js - 3) until PV(js - 3) has read it
+        if (js >= kNSB) bar_wait(b_pv + 8 * (js % kNSB), ((js - kNSB) / kNSB) & 1u);
         PROF_MARK(1);
+        if (lane == 0) TTS_TR(js, 1);
         tc_fence_after();
-        // S[128 x 32] = Q . K^T for both pages of the unit: 8 MMAs of N = 32 (an
-        // absent second page leaves columns 16..31 undefined; they are masked)
-        const uint32_t sd = t_s + (js & 1) * kSCols;
-        const uint64_t dk = dk0 + (uint64_t)((slot * kSlot) >> 4);
+        // S[128 x 128] = Q . K^T over the unit's 8 pages: 8 MMAs (K = 16 of d
+        // each; an absent page leaves its 16 columns undefined: masked)
+        const uint32_t sd = t_s + (js % kNSB) * kSCols;
+        const uint64_t dk = dk0 + (uint64_t)((slot * kKSlot) >> 4);
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ts(sd, t_q + ks * 8, dk + (uint64_t)(((ks >> 2) * kTile + (ks & 3) * 32) >> 4), id_s, ks > 0);
-          tc_commit(b_sfull + 8 * (js & 1));
+            mma_ss(sd, dq0 + (uint64_t)(((ks >> 2) * (kRows * 128) + (ks & 3) * 32) >> 4),
+                   dk + (uint64_t)(((ks >> 2) * (kKSlot / 2) + (ks & 3) * 32) >> 4), id_s, ks > 0);
+          tc_commit(b_sfull + 8 * (js % kNSB));
+          tc_commit(b_kempty + 8 * slot);
         }
         __syncwarp();
-        if (lane == 0) TTS_TR(js, 7);
+        if (lane == 0) TTS_TR(js, 2);
       }
     }
     PROF_MARK(2);
-    PROF_FLUSH(5);
-  } else if (warp == 6) {
+    PROF_FLUSH(10);
+  } else if (warp == 11) {
     // ====================== PV issuer: O += P V ======================
     constexpr uint32_t id_pv = idesc_f16(kRows, kD, true);
-    const uint64_t dv0 = sdesc(base + kOffRing, 2048, 1024, 2);  // V tiles: MN-major SW128
+    const uint64_t dv0 = sdesc(base + kOffV, 2048, 1024, 2);  // V tiles: MN-major SW128
     // (TTS_PROF: [0] waiting for V, [1] waiting for P, [2] waiting for O, [3] issuing)
     PROF_DECL;
     int js = 0;
@@ -667,42 +710,49 @@ __global__ void __launch_bounds__(kThreads, 2)
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
       for (int j = j0; j < j1; ++j, ++js) {
-        const int slot = js % kNS;
+        const int slot = js % kNV;
         PROF_MARK(3);
-        bar_wait(b_full + 8 * slot, (js / kNS) & 1u);
+        bar_wait(b_vfull + 8 * slot, (js / kNV) & 1u);
         PROF_MARK(0);
-        bar_wait(b_pfull + 8 * (js & 1), (js >> 1) & 1u);
+        if (lane == 0) TTS_TR(js, 6);
+        bar_wait(b_pfull + 8 * (js % kNSB), (js / kNSB) & 1u);
         PROF_MARK(1);
+        if (lane == 0) TTS_TR(js, 7);
         // the first PV of a piece overwrites O: the previous piece's epilogue must have read it
         if (j == j0 && pc > 0) bar_wait(b_ofree, (pc - 1) & 1);
         PROF_MARK(2);
-        if (lane == 0) TTS_TR(js, 2);
         tc_fence_after();
-        const uint32_t pa = t_s + (js & 1) * kSCols;
+        const uint32_t pa = t_s + (js % kNSB) * kSCols;
+        const int4* mrow = meta + (js % kNM) * kU;
         const bool e = elect_one();
         uint32_t acc = j != j0;
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
-          if (meta[slot * kU + k].x < 0) continue;
-          const uint64_t dv = dv0 + (uint64_t)((slot * kSlot + (kU + k) * kTile) >> 4);
+          if (mrow[k].x < 0) continue;
+          const uint64_t dv = dv0 + (uint64_t)((slot * kVSlot + k * kTile) >> 4);
           if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
           acc = 1;
         }
         if (e) {
-          // S(js) completed before the softmax produced P(js), so this commit
-          // covers every read of the slot
-          tc_commit(b_empty + 8 * slot);
-          tc_commit(b_pv + 8 * (js & 1));
-          TTS_TR(js, 3);
+          tc_commit(b_vempty + 8 * slot);
+          tc_commit(b_pv + 8 * (js % kNSB));
         }
         __syncwarp();
       }
     }
     PROF_MARK(3);
-    PROF_FLUSH(6);
-  } else if (warp < 4) {
-    // ============================ softmax (warps 0-3) ============================
-    if (n_pieces > 0 && n1 == 0) {  // first piece in phase 2: Q after the plan
+    PROF_FLUSH(11);
+  } else {
+    // ==================== softmax (warps 0-7: lane quadrant warp & 3, half hh) ====================
+    // The two warps of a quadrant hold the same 32 rows: warp half hh reads the
+    // S columns of pages [4 hh, 4 hh + 4) of every unit and owns O columns
+    // [64 hh, 64 hh + 64) (rescale, epilogue, merge).  The row max is
+    // exchanged through shared memory (one pair barrier per unit), so both
+    // halves use the same running max; each keeps its own partial row sum.
+    const int hh = warp >> 2;
+    const int pair_bar = 2 + (warp & 3);  // named barrier of the quadrant's two warps
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    if (n_pieces > 0) {  // the first piece's Q (the schedule needs the plan)
       int gi, slab, j0, j1, pslot;
       piece(0, gi, slab, j0, j1, pslot);
       load_q(gi, slab);
@@ -720,131 +770,140 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int lrel = slab / p.Hkv, kh = slab % p.Hkv;
       float m_ref = -1e30f, l = 0.f;
       for (int j = j0; j < j1; ++j, ++js) {
-        if (r == 0) TTS_TR(js, 4);
         PROF_MARK(3);
-        bar_wait(b_sfull + 8 * (js & 1), (js >> 1) & 1u);
+        bar_wait(b_sfull + 8 * (js % kNSB), (js / kNSB) & 1u);
         PROF_MARK(0);
         PROF_CNT(7);
-        if (r == 0) TTS_TR(js, 5);
+        if (lane == 0 && warp == 0) TTS_TR(js, 3);
+        if (lane == 0 && warp == 5) TTS_TR2(js, 0);
         tc_fence_after();
-        const int slot = js % kNS;
-        int4 mt[kU];
-        bool mem[kU], wm[kU];
-        bool wany = false;
+        const int4* mrow = meta + (js % kNM) * kU + hh * kUH;
+        const uint32_t tB = t_s + lane_off + (js % kNSB) * kSCols;  // this unit's S/P buffer
+        const uint32_t tS = tB + hh * (kUH * kP);
+        // page membership: bit k of lm = this row reads page kUH hh + k; wmask =
+        // the warp's union (a page none of its rows reads: P = 0, no exponentials)
+        uint32_t lm = 0;
 #pragma unroll
-        for (int k = 0; k < kU; ++k) {
-          mt[k] = meta[slot * kU + k];
-          // warp-uniform page membership: a warp none of whose rows reads a
-          // page skips its exponentials (P = 0 there)
-          mem[k] = mt[k].x >= 0 && rvalid && ((((uint32_t)mt[k].y) >> rbl) & 1u);
-          wm[k] = __any_sync(0xffffffffu, mem[k]);
-          wany |= wm[k];
+        for (int k = 0; k < kUH; ++k) {
+          const int4 mt = mrow[k];
+          lm |= (mt.x >= 0 && rvalid && ((((uint32_t)mt.y) >> rbl) & 1u)) ? 1u << k : 0u;
         }
-        uint32_t pk[kSCols / 2];
+        const uint32_t wmask = __reduce_or_sync(0xffffffffu, lm);
+        uint32_t sr[kUH / 2][32];
+        float mx = -INFINITY;
+        if (wmask) {
+          // S columns of the page pairs this warp reads
 #pragma unroll
-        for (int i = 0; i < kSCols / 2; ++i) pk[i] = 0u;
-        if (wany) {
-          float v[kSCols];
-          {
-            // only the pages this warp's rows read: TMEM read bandwidth is a
-            // shared per-SM resource (a private page is read by one warp)
-            uint32_t sr[kSCols];
-            if (wm[0] && wm[1]) {
-              tc_ld32(t_s + lane_off + (js & 1) * kSCols, sr);
-              tc_wait_ld();
+          for (int q = 0; q < kUH / 2; ++q)
+            if ((wmask >> (2 * q)) & 3u) tc_ld32(tS + 32 * q, sr[q]);
+          tc_wait_ld();
+        }
+        if (wmask) {
+          // raw scores (scale > 0 commutes with max); token slots >= ntok -> -inf
+          // (partial pages only); rows not reading page k: max and exponent
+          // offset -inf below (P exactly 0)
 #pragma unroll
-              for (int i = 0; i < kSCols; ++i) v[i] = __uint_as_float(sr[i]);
-            } else {
-              const int pg = wm[0] ? 0 : 1;
-              tc_ld16(t_s + lane_off + (js & 1) * kSCols + pg * kP, *reinterpret_cast<uint32_t(*)[kP]>(sr));
-              tc_wait_ld();
+          for (int k = 0; k < kUH; ++k) {
+            if (!((wmask >> k) & 1u)) continue;
+            uint32_t* w = sr[k >> 1] + (k & 1) * kP;
+            const int ntok = mrow[k].z;
+            if (ntok < kP) {
 #pragma unroll
-              for (int i = 0; i < kP; ++i) {
-                v[i] = pg == 0 ? __uint_as_float(sr[i]) : -INFINITY;
-                v[kP + i] = pg == 1 ? __uint_as_float(sr[i]) : -INFINITY;
-              }
+              for (int c = 0; c < kP; ++c) w[c] = c < ntok ? w[c] : __float_as_uint(-INFINITY);
             }
+            float mk = fmax3(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]));
+#pragma unroll
+            for (int c = 3; c + 1 < kP; c += 2) mk = fmax3(mk, __uint_as_float(w[c]), __uint_as_float(w[c + 1]));
+            mk = fmaxf(mk, __uint_as_float(w[kP - 1]));
+            mx = fmaxf(mx, ((lm >> k) & 1u) ? mk : -INFINITY);
           }
-          // raw scores (scale > 0 commutes with max); rows not reading page k
-          // are masked once per page (max -> -inf, exponent offset -> -inf, so
-          // P is exactly 0); token slots >= ntok only on a partial page
-          float mx = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < kU; ++k) {
-            if (mt[k].x >= 0 && mt[k].z < kP) {
-#pragma unroll
-              for (int c = 0; c < kP; ++c)
-                if (c >= mt[k].z) v[k * kP + c] = -INFINITY;
-            }
-            const float* w = v + k * kP;
-            float mk = fmax3(w[0], w[1], w[2]);
-#pragma unroll
-            for (int c = 3; c + 1 < kP; c += 2) mk = fmax3(mk, w[c], w[c + 1]);
-            mk = fmaxf(mk, w[kP - 1]);
-            mx = fmaxf(mx, mem[k] ? mk : -INFINITY);
-          }
-          mx *= p.scale_log2;
-          const bool need = mx > m_ref + 8.0f;
-          if (__any_sync(0xffffffffu, need) && j > j0) {
-            if (r == 0) TTS_TR2(js, 7);
-            PROF_MARK(1);
-            // every earlier PV product must have landed before O is rescaled in TMEM
-            bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
-            tc_fence_after();
-            const float alpha = need ? exp2f(m_ref - mx) : 1.f;
+        }
+        // the unit's row max over both halves (the barrier also orders the
+        // other half's P stores, which overlap these S columns, after our loads)
+        float* xm = s_xm + ((js & 1) * 2 + hh) * kRows;
+        xm[r] = mx;
+        tc_fence_before();
+        pair_sync();
+        tc_fence_after();
+        if (lane == 0 && warp == 0) TTS_TR(js, 4);
+        if (lane == 0 && warp == 5) TTS_TR2(js, 1);
+        mx = fmaxf(mx, s_xm[((js & 1) * 2 + (hh ^ 1)) * kRows + r]) * p.scale_log2;
+        const bool need = mx > m_ref + 8.0f;
+        if (__any_sync(0xffffffffu, need) && j > j0) {
+          PROF_MARK(1);
+          // every earlier PV product must have landed before O is rescaled in TMEM
+          bar_wait(b_pv + 8 * ((js - 1) % kNSB), ((js - 1) / kNSB) & 1u);
+          tc_fence_after();
+          const float alpha = need ? exp2f(m_ref - mx) : 1.f;
 #pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-              uint32_t o[32];
-              tc_ld32(t_o + lane_off + ch * 32, o);
-              tc_wait_ld();
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t o[32];
+            const uint32_t ta = t_o + lane_off + hh * 64 + ch * 32;
+            tc_ld32(ta, o);
+            tc_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tc_st32(t_o + lane_off + ch * 32, o);
-            }
-            tc_wait_st();
-            l *= alpha;
-            PROF_MARK(4);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tc_st32(ta, o);
           }
-          if (need) m_ref = mx;
+          tc_wait_st();
+          l *= alpha;
+          PROF_MARK(4);
+        }
+        if (need) m_ref = mx;
+        if (wmask) {
           const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
           float2 lacc = make_float2(0.f, 0.f);
+          // P (fp16, value c of page k at column 8k + c/2) over the pair's S
+          // columns; every S load above has completed
 #pragma unroll
-          for (int k = 0; k < kU; ++k) {
-            if (wm[k]) {
-              const float nm = mem[k] ? -m_ref : -INFINITY;
-              const float2 nm2 = make_float2(nm, nm);
+          for (int q = 0; q < kUH / 2; ++q) {
+            uint32_t pk[kP];
 #pragma unroll
-              for (int c = 0; c < kP; c += 2) {
-                const float2 x = ffma2(make_float2(v[k * kP + c], v[k * kP + c + 1]), sc2, nm2);
-                float a, b;
-                if (kPoly == 2 || (kPoly == 1 && ((c >> 1) & 1))) {
-                  const float2 e2 = ex2_poly2(x);
-                  a = e2.x;
-                  b = e2.y;
-                } else {
-                  a = ex2(x.x);
-                  b = ex2(x.y);
+            for (int h = 0; h < 2; ++h) {
+              const int k = 2 * q + h;
+              if ((wmask >> k) & 1u) {
+                const float nm = ((lm >> k) & 1u) ? -m_ref : -INFINITY;
+                const float2 nm2 = make_float2(nm, nm);
+                const uint32_t* w = sr[q] + h * kP;
+#pragma unroll
+                for (int c = 0; c < kP; c += 2) {
+                  const float2 x = ffma2(make_float2(__uint_as_float(w[c]), __uint_as_float(w[c + 1])), sc2, nm2);
+                  float a, b;
+                  if (kPoly == 2 || (kPoly == 1 && ((c >> 1) & 1))) {
+                    const float2 e2 = ex2_poly2(x);
+                    a = e2.x;
+                    b = e2.y;
+                  } else {
+                    a = ex2(x.x);
+                    b = ex2(x.y);
+                  }
+                  lacc = fadd2(lacc, make_float2(a, b));
+                  pk[h * (kP / 2) + c / 2] = pack_f16x2(a, b);
                 }
-                lacc = fadd2(lacc, make_float2(a, b));
-                pk[(k * kP + c) / 2] = pack_f16x2(a, b);
+              } else {
+#pragma unroll
+                for (int c = 0; c < kP / 2; ++c) pk[h * (kP / 2) + c] = 0u;
               }
             }
+            tc_st16(tB + hh * (kUH * kP / 2) + 16 * q, pk);
           }
           l += lacc.x + lacc.y;
           PROF_MARK(1);
           PROF_CNT(6);
         } else {
+          uint32_t z[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) z[i] = 0u;
+          tc_st32(tB + hh * (kUH * kP / 2), z);
           PROF_MARK(2);
         }
-        // P (fp16) over the unit's first 16 S columns (value c at column c/2)
-        tc_st16(t_s + lane_off + (js & 1) * kSCols, pk);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (r == 0) TTS_TR(js, 6);
-        if (lane == 0) TTS_TR2(js, warp);
-        if (lane == 0) bar_arrive(b_pfull + 8 * (js & 1));
+        if (lane == 0) bar_arrive(b_pfull + 8 * (js % kNSB));
         PROF_MARK(5);
+        if (lane == 0 && warp == 0) TTS_TR(js, 5);
+        if (lane == 0 && warp == 5) TTS_TR2(js, 2);
       }
       // the next piece's Q (every S MMA of this piece has completed), so that
       // its S = Q K^T overlaps this piece's epilogue
@@ -861,132 +920,146 @@ __global__ void __launch_bounds__(kThreads, 2)
       // writes nothing)
       const int tu = s_pre[gi + 1] - s_pre[gi];
       if (j1 > j0) {
-      bar_wait(b_pv + 8 * ((js - 1) & 1), ((js - 1) >> 1) & 1u);
-      PROF_MARK(9);
-      tc_fence_after();
-      float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD;
-      if (j0 == 0 && j1 == tu) {
-        const float inv = 1.f / l;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t o[32];
-          tc_ld32(t_o + lane_off + ch * 32, o);
-          tc_wait_ld();
+        // the row sum over both halves (the partner's partial sum of this piece)
+        // (row sums through the max-exchange buffer of the next unit's parity:
+        // its last reader passed the pair barrier of unit js - 1)
+        float* s_xl = s_xm + (js & 1) * 2 * kRows;
+        s_xl[hh * kRows + r] = l;
+        bar_wait(b_pv + 8 * ((js - 1) % kNSB), ((js - 1) / kNSB) & 1u);
+        PROF_MARK(9);
+        tc_fence_after();
+        // this half's 64 O columns -> registers; the accumulator is released at
+        // once, so the next piece's first PV overlaps the stores below
+        uint32_t o[2][32];
+        tc_ld32(t_o + lane_off + hh * 64, o[0]);
+        tc_ld32(t_o + lane_off + hh * 64 + 32, o[1]);
+        tc_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(b_ofree);
+        pair_sync();
+        l += s_xl[(hh ^ 1) * kRows + r];
+        pair_sync();  // s_xl is rewritten by the next unit's max exchange
+        float* orow = p.out + ((((int64_t)lrel * p.n_call + g.call_idx) * p.maxB + g.beam0 + rbl) * p.Hq + kh * G + rh) * kD + hh * 64;
+        if (j0 == 0 && j1 == tu) {
+          const float inv = 1.f / l;
           if (rvalid) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(orow + ch * 32 + i) =
-                  make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
-                              __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+            for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(orow + c2 * 32 + i) =
+                    make_float4(__uint_as_float(o[c2][i]) * inv, __uint_as_float(o[c2][i + 1]) * inv,
+                                __uint_as_float(o[c2][i + 2]) * inv, __uint_as_float(o[c2][i + 3]) * inv);
+          }
+        } else {
+          // a5: this piece's (m, l, unnormalised O) -> its partial slot (2c for the
+          // CTA's first phase-2 piece, 2c + 1 for its last); O chunk-major ([32
+          // chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
+          // The last piece to finish merges.
+          float* part = p.partial + (size_t)pslot * kPartFloats;
+          if (hh == 0) {
+            part[r] = m_ref;
+            part[kRows + r] = l;
+          }
+          float4* po = reinterpret_cast<float4*>(part + 2 * kRows) + r;
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              __stcg(po + ((2 * hh + c2) * 8 + i) * kRows,
+                     make_float4(__uint_as_float(o[c2][4 * i]), __uint_as_float(o[c2][4 * i + 1]),
+                                 __uint_as_float(o[c2][4 * i + 2]), __uint_as_float(o[c2][4 * i + 3])));
+          __threadfence();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const int64_t T0 = F(slab * ng + gi);
+          auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
+            if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
+            int lo = 0, hi = C2;  // largest c with start2(c) <= x
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (start2(mid) <= x) lo = mid;
+              else hi = mid;
+            }
+            return lo;
+          };
+          const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
+          const int tile = slab * ng + gi;
+          if (threadIdx.x == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          PROF_MARK(10);
+          if (s_info[0]) {
+            __threadfence();
+            const int np = c_last - c_first + 1;
+            // piece k's slot: only the first CTA's range can start before the tile
+            const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
+            auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
+            // latency-bound (L2 round trips under full HBM load): every batch of
+            // loads is issued before any is consumed
+            float M = -INFINITY, L = 0.f;
+            for (int k0 = 0; k0 < np; k0 += 8) {
+              float mv[8], lv[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const bool ok = k0 + i < np;
+                mv[i] = ok ? __ldcg(part_of(k0 + i) + r) : -INFINITY;
+                lv[i] = ok ? __ldcg(part_of(k0 + i) + kRows + r) : 0.f;
+              }
+              float M2 = M;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) M2 = fmaxf(M2, mv[i]);
+              L *= exp2f(M - M2);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) L += k0 + i < np ? exp2f(mv[i] - M2) * lv[i] : 0.f;
+              M = M2;
+            }
+            const float inv = 1.f / L;
+#pragma unroll 1
+            for (int c2 = 0; c2 < 2; ++c2) {
+              const int ch = 2 * hh + c2;
+              float4 acc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int k = 0; k < np; k += 2) {
+                const bool two = k + 1 < np;
+                const float* pa = part_of(k);
+                const float* pb = part_of(two ? k + 1 : k);
+                const float wa = __ldcg(pa + r), wb = __ldcg(pb + r);
+                const float4* sa = reinterpret_cast<const float4*>(pa + 2 * kRows) + r;
+                const float4* sb = reinterpret_cast<const float4*>(pb + 2 * kRows) + r;
+                float4 xa[8], xb[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  xa[i] = __ldcg(sa + (ch * 8 + i) * kRows);
+                  xb[i] = __ldcg(sb + (ch * 8 + i) * kRows);
+                }
+                const float fa = exp2f(wa - M), fb = two ? exp2f(wb - M) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  acc[i].x += fa * xa[i].x + fb * xb[i].x;
+                  acc[i].y += fa * xa[i].y + fb * xb[i].y;
+                  acc[i].z += fa * xa[i].z + fb * xb[i].z;
+                  acc[i].w += fa * xa[i].w + fb * xb[i].w;
+                }
+              }
+              if (rvalid) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  *reinterpret_cast<float4*>(orow + c2 * 32 + 4 * i) =
+                      make_float4(acc[i].x * inv, acc[i].y * inv, acc[i].z * inv, acc[i].w * inv);
+              }
+            }
+            if (threadIdx.x == 0) p.tile_cnt[tile] = 0;  // every piece of the tile has arrived: ready for the next call
+            PROF_MARK(11);
+            PROF_CNT(12);
           }
         }
       } else {
-        // a5: this piece's (m, l, unnormalised O) -> its partial slot (2c for the
-        // CTA's first phase-2 piece, 2c + 1 for its last); O stored chunk-major
-        // ([32 chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
-        // The last piece to finish merges.
-        float* part = p.partial + (size_t)pslot * kPartFloats;
-        part[r] = m_ref;
-        part[kRows + r] = l;
-        float4* po = reinterpret_cast<float4*>(part + 2 * kRows) + r;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t o[32];
-          tc_ld32(t_o + lane_off + ch * 32, o);
-          tc_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            __stcg(po + (ch * 8 + i) * kRows,
-                   make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
-                               __uint_as_float(o[4 * i + 3])));
-        }
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int64_t T0 = F(slab * ng + gi);
-        auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
-          if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
-          int lo = 0, hi = C2;  // largest c with start2(c) <= x
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (start2(mid) <= x) lo = mid;
-            else hi = mid;
-          }
-          return lo;
-        };
-        const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
-        const int tile = slab * ng + gi;
-        if (r == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        PROF_MARK(10);
-        if (s_info[0]) {
-          __threadfence();
-          const int np = c_last - c_first + 1;
-          // piece k's slot: only the first CTA's range can start before the tile
-          const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
-          auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
-          // latency-bound (L2 round trips under full HBM load): every batch of
-          // loads is issued before any is consumed
-          float M = -INFINITY, L = 0.f;
-          for (int k0 = 0; k0 < np; k0 += 8) {
-            float mv[8], lv[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const bool ok = k0 + i < np;
-              mv[i] = ok ? __ldcg(part_of(k0 + i) + r) : -INFINITY;
-              lv[i] = ok ? __ldcg(part_of(k0 + i) + kRows + r) : 0.f;
-            }
-            float M2 = M;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) M2 = fmaxf(M2, mv[i]);
-            L *= exp2f(M - M2);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) L += k0 + i < np ? exp2f(mv[i] - M2) * lv[i] : 0.f;
-            M = M2;
-          }
-          const float inv = 1.f / L;
-#pragma unroll 1
-          for (int ch = 0; ch < 4; ++ch) {
-            float4 acc[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int k = 0; k < np; k += 2) {
-              const bool two = k + 1 < np;
-              const float* pa = part_of(k);
-              const float* pb = part_of(two ? k + 1 : k);
-              const float wa = __ldcg(pa + r), wb = __ldcg(pb + r);
-              const float4* sa = reinterpret_cast<const float4*>(pa + 2 * kRows) + r;
-              const float4* sb = reinterpret_cast<const float4*>(pb + 2 * kRows) + r;
-              float4 xa[8], xb[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                xa[i] = __ldcg(sa + (ch * 8 + i) * kRows);
-                xb[i] = __ldcg(sb + (ch * 8 + i) * kRows);
-              }
-              const float fa = exp2f(wa - M), fb = two ? exp2f(wb - M) : 0.f;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                acc[i].x += fa * xa[i].x + fb * xb[i].x;
-                acc[i].y += fa * xa[i].y + fb * xb[i].y;
-                acc[i].z += fa * xa[i].z + fb * xb[i].z;
-                acc[i].w += fa * xa[i].w + fb * xb[i].w;
-              }
-            }
-            if (rvalid) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                *reinterpret_cast<float4*>(orow + ch * 32 + 4 * i) =
-                    make_float4(acc[i].x * inv, acc[i].y * inv, acc[i].z * inv, acc[i].w * inv);
-            }
-          }
-          if (r == 0) p.tile_cnt[tile] = 0;  // every piece of the tile has arrived: ready for the next call
-          PROF_MARK(11);
-          PROF_CNT(12);
-        }
+        // an empty piece read nothing from O: release it for the next piece
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(b_ofree);
       }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) bar_arrive(b_ofree);  // the next piece's first PV may overwrite O
     }
     PROF_MARK(3);
     PROF_FLUSH(warp);
@@ -998,6 +1071,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
   if (threadIdx.x == 0) TTS_CTA(2, gtimer());
+  if (threadIdx.x == 0) TTS_SPAN(p.launch_id, 1, gtimer(), atomicMax);
 #ifdef TTS_TRACE
   if (threadIdx.x == 0) {
     unsigned smid;
@@ -1010,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     TTS_CTA(3, units | ((long long)smid << 32));
   }
 #endif
-  if (warp == 5) {
+  if (warp == 10) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
@@ -1030,9 +1104,21 @@ extern "C" int tts_debug_read_trace(long long* out_h) {
   e = e ? e : (int)cudaMemcpyFromSymbol(out_h + 1024 * 8, g_trace2, sizeof(g_trace2));
   return e ? e : (int)cudaMemcpyFromSymbol(out_h + 2 * 1024 * 8, g_cta, sizeof(g_cta));
 }
+// launch spans: reset (min slots to ~0, max slots to 0) / read [32768][4]
+extern "C" int tts_debug_reset_spans() {
+  static unsigned long long h[32768][4];
+  for (int i = 0; i < 32768; ++i) h[i][0] = h[i][2] = ~0ull, h[i][1] = h[i][3] = 0;
+  return (int)cudaMemcpyToSymbol(g_lspan, h, sizeof(h));
+}
+extern "C" int tts_debug_read_spans(unsigned long long* out_h) {
+  return (int)cudaMemcpyFromSymbol(out_h, g_lspan, sizeof(g_lspan));
+}
 #endif
 
-size_t umma_partial_bytes() { return (size_t)2 * kMaxCtas * kPartFloats * 4; }
+// split tiles' partial states, then the per-CTA unit-prefix scratch
+size_t umma_partial_bytes() {
+  return (size_t)2 * kMaxCtas * kPartFloats * 4 + (size_t)kMaxCtas * (kMaxGroups + 1) * 4;
+}
 int umma_max_groups() { return kMaxGroups; }
 
 bool umma_supported(const Ctx* c) {
@@ -1042,8 +1128,8 @@ bool umma_supported(const Ctx* c) {
 }
 
 // Per device context: the kernel attributes, and the residency argument the
-// plan's double buffer relies on.  The grid is exactly two CTAs per SM and at
-// most two fit per SM (static_assert on the shared memory below), so all CTAs
+// plan's double buffer relies on.  The grid is exactly one CTA per SM and at
+// most one fits per SM (static_assert on the shared memory above), so all CTAs
 // of call N+1 being resident implies call N's attention kernel has exited --
 // and call N+2's k_plan (PDL-released by call N+1's CTAs) can only then
 // overwrite the plan buffer call N read.  A device with more SMs than the
@@ -1055,14 +1141,14 @@ cudaError_t umma_prepare(Ctx* c) {
   for (auto k : {k_tree_umma<0>, k_tree_umma<1>, k_tree_umma<2>}) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
-    // two CTAs per SM need 2 x kSmemBytes (> the 164 KB carveout step): ask for the largest
+    // the whole shared-memory carveout
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, kSmemBytes);
     if (e != cudaSuccess) return e;
     c->umma_occupancy = occ;  // diagnostics only (the occupancy API under-reports with the carveout hint)
-    if (2 * c->num_sms > kMaxCtas) return cudaSuccess;
+    if (c->num_sms > kMaxCtas) return cudaSuccess;
   }
   c->umma_ok = true;
   return cudaSuccess;
@@ -1099,6 +1185,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   pp.maxB = c->cfg.max_beams;
   pp.maxP = c->cfg.max_pages_per_beam;
   pp.num_pages = c->cfg.num_pages;
+  pp.launch_id = (int)c->launches;
 
   UParams p;
   p.items = pp.items;
@@ -1117,11 +1204,13 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.n_layers = n_layers;
   p.n_groups = n_groups;
   p.partial = c->ws_partial;
+  p.pre = reinterpret_cast<int*>(c->ws_partial + (size_t)2 * kMaxCtas * kPartFloats);
   p.tile_cnt = c->ws_tile_cnt;
   p.num_pages = c->cfg.num_pages;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.round_robin = c->env_round_robin;
   p.split_partial_round = c->env_split_partial;
+  p.launch_id = (int)c->launches;
   UInline inl;  // host staging of the parameter block (copied by the launch)
   if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {
     std::memcpy(inl.g, groups_h, (size_t)n_groups * sizeof(GroupDesc));
@@ -1155,8 +1244,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  // persistent: two CTAs per SM (the smem / TMEM / register budget of one CTA)
-  cfg.gridDim = dim3(2 * c->num_sms);  // persistent: two CTAs per SM (<= kMaxCtas, umma_prepare)
+  cfg.gridDim = dim3(c->num_sms);  // persistent: one CTA per SM (<= kMaxCtas, umma_prepare)
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;

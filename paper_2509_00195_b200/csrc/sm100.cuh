@@ -15,6 +15,15 @@ __device__ __forceinline__ void bar_init(uint32_t b, int n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(n));
 }
 __device__ __forceinline__ void bar_wait(uint32_t b, uint32_t par) {
+#ifdef TTS_WAIT_NOHINT
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(b),
+      "r"(par)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "W_%=:\n\t"
@@ -22,6 +31,7 @@ __device__ __forceinline__ void bar_wait(uint32_t b, uint32_t par) {
       "@!p bra W_%=;\n}" ::"r"(b),
       "r"(par)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bar_arrive(uint32_t b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");

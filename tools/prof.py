@@ -31,10 +31,10 @@ cfg = workload.CONFIGS[name].with_(n_steps=steps)
 r = BeamStepRunner(cfg)
 r.run()
 torch.cuda.synchronize()
-buf = np.zeros(512 * 8 * 16, dtype=np.int64)
+buf = np.zeros(512 * 12 * 16, dtype=np.int64)
 tts.load().tts_debug_read_prof(buf.ctypes.data_as(ctypes.c_void_p))
-pr = buf.reshape(512, 8, 16)
-n_cta = int((pr[:, 5, :].sum(1) > 0).sum())
+pr = buf.reshape(512, 12, 16)
+n_cta = int((pr[:, 10, :].sum(1) > 0).sum())
 pr = pr[:n_cta]
 units = pr[:, 0, 7].astype(float)
 print(f"{name} {extra}: {n_cta} CTAs, units per CTA median {np.median(units):.0f} (min {units.min():.0f}, max {units.max():.0f})")
@@ -43,17 +43,18 @@ print(f"  softmax warp total cycles median {np.median(tot):.0f}  -> cycles per u
 names = {
     "softmax": ["wait S", "member softmax", "skipped", "other", "rescale", "P store+arrive", "", "", "load Q",
                 "wait last PV", "O store / partial", "merge"],
-    "producer": ["wait slot", "issue", "item loads"],
+    "K producer": ["wait slot", "issue", "item loads"],
+    "V producer": ["wait slot", "issue", "item loads"],
     "S": ["wait K", "wait S buf", "issue", "wait Q"],
     "PV": ["wait V", "wait P", "wait O", "issue"],
 }
-for w in range(4):
+for w in range(8):
     x = pr[:, w, :6] / np.maximum(units, 1)[:, None]
     mem = np.median(pr[:, w, 6] / np.maximum(units, 1))
     x = pr[:, w, :12] / np.maximum(units, 1)[:, None]
     print(f"  softmax warp {w}: member fraction {mem:.2f}; " +
           ", ".join(f"{n} {np.median(x[:, k]):.0f}" for k, n in enumerate(names["softmax"]) if n))
 print(f"  merges per CTA (warp 0) mean {pr[:, 0, 12].mean():.2f}")
-for w, role in ((4, "producer"), (5, "S"), (6, "PV")):
+for w, role in ((8, "K producer"), (9, "V producer"), (10, "S"), (11, "PV")):
     x = pr[:, w, :len(names[role])] / np.maximum(units, 1)[:, None]
     print(f"  {role:8s} warp {w}: " + ", ".join(f"{n} {np.median(x[:, k]):.0f}" for k, n in enumerate(names[role])))

@@ -33,41 +33,32 @@ if len(cta):
     dur = ex - st
     print(f"  CTA duration min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us; us per unit (median) {np.median(dur / np.maximum(un, 1)):.3f};"
           f" epilogue (exit - loop end) median {np.median(ex - le):.2f} us; distinct SMs {len(set(sm.tolist()))}")
+    bid = np.nonzero(buf[2 * 1024 * 8:].reshape(4096, 4)[:, 0] > 0)[0]
+    rate = dur / np.maximum(un, 1)
+    print("  us per unit by CTA half: blockIdx < 148: %.3f, >= 148: %.3f" % (np.median(rate[bid < 148]), np.median(rate[bid >= 148])))
+    order = np.argsort(sm)
+    print("  us per unit by SM id (pairs of co-resident CTAs averaged), 16 per row:")
+    per_sm = {}
+    for s_, r_ in zip(sm.tolist(), rate.tolist()):
+        per_sm.setdefault(s_, []).append(r_)
+    ks = sorted(per_sm)
+    for i in range(0, len(ks), 16):
+        print("   ", " ".join(f"{np.mean(per_sm[k]):.3f}" for k in ks[i:i + 16]))
     hist = np.histogram(ex, bins=10)
     print("  exit-time histogram:", hist[0].tolist(), "edges", [round(x, 1) for x in hist[1].tolist()])
-n = int((tr[:, 4] > 0).sum())
-t0 = tr[0, 4]
-print("units", n)
-e = tr[1023]
-print("CTA: start->prologue", e[1] - e[0], "prologue->loop end", e[2] - e[1], "loop end->exit", e[3] - e[2], "total", e[3] - e[0])
-print("j: mma_fullwait_start mma_fullwait_end mma_pfull_end mma_pv_commit | sm_wait_start sm_sfull_end sm_arrive (cycles rel)")
-for j in range(min(n, 40)):
-    e = tr[j] - t0
-    print(j, e[0], e[1], e[2], e[3], "|", e[4], e[5], e[6], " softmax_busy", tr[j, 6] - tr[j, 5], " waitS", tr[j, 5] - tr[j, 4])
-tr[1023] = 0
-d = tr[1:n, 5] - tr[:n - 1, 5]
-print("median cycles per unit", np.median(d), "softmax busy median", np.median(tr[:n, 6] - tr[:n, 5]),
-      "sfull wait median", np.median(tr[:n, 5] - tr[:n, 4]), "mma pfull-wait median", np.median(tr[:n, 2] - tr[:n, 1]))
-
-print("per-warp P arrive (rel. to warp 0) and MMA pfull_end (rel. to last warp), first 12 units:")
-for j in range(min(n, 12)):
-    a = t2[j, :4]
-    print(j, [int(x - a[0]) for x in a], "mma_pfull_end - last_arrive", int(tr[j, 2] - a.max()))
-print("median S-issue cycles (fullwait_end -> issue_s done):", np.median(tr[:n-1, 7] - tr[:n-1, 1]),
-      " issue_s done -> pfull_end:", np.median(tr[:n-1, 2] - tr[:n-1, 7]), " pfull_end -> pv_commit:", np.median(tr[:n-1, 3] - tr[:n-1, 2]),
-      " pv_commit -> next fullwait_start:", np.median(tr[1:n, 0] - tr[:n-1, 3]))
-d = t2[:n, :4] - t2[:n, :1]
-print("median arrive offsets vs warp 0:", np.median(d, axis=0), " median pfull_end - last arrive:", np.median(tr[:n, 2] - t2[:n, :4].max(1)))
-full = []
-print("member units", len(full), "of", n)
-if full:
-    f = np.array(full)
-    print("member path medians: meta->ld", np.median(t2[f, 1] - t2[f, 0]), "ld->max", np.median(t2[f, 2] - t2[f, 1]),
-          "max->exp_done", np.median(t2[f, 3] - t2[f, 2]), "exp->st_done", np.median(t2[f, 4] - t2[f, 3]),
-          "st->arrive", np.median(tr[f, 6] - t2[f, 4]), "sfull->meta", np.median(t2[f, 0] - tr[f, 5]),
-          "rescales", int((t2[f, 7] > 0).sum()))
-sk = [j for j in range(n) if t2[j, 3] == 0]
-if sk:
-    s_ = np.array(sk)
-    print("skip path medians: sfull->meta", np.median(t2[s_, 0] - tr[s_, 5]), "meta->st_done", np.median(t2[s_, 4] - t2[s_, 0]),
-          "st->arrive", np.median(tr[s_, 6] - t2[s_, 4]))
+n = int((tr[:, 3] > 0).sum())
+print("units traced", n)
+t0 = tr[0, 0]
+ev = ["S kfull", "S sbuf", "S issued", "sm0 sfull", "sm0 pair", "sm0 arrive", "PV vfull", "PV pfull"]
+ev2 = ["sm5 sfull", "sm5 pair", "sm5 arrive", "Kprod slot", "Vprod slot"]
+print("j | " + " ".join(f"{e:>10s}" for e in ev + ev2))
+for j in list(range(0, min(n, 12))) + list(range(max(12, n // 2), min(n, n // 2 + 12))):
+    print(j, "|", " ".join(f"{int(x - t0):10d}" for x in list(tr[j]) + list(t2[j, :5])))
+lo, hi = max(1, n // 4), max(2, 3 * n // 4)
+d = lambda a, b: np.median(a[lo:hi] - b[lo:hi])
+print("median per unit period (sm0 sfull):", np.median(np.diff(tr[lo:hi, 3])))
+print("median: S kfull->sbuf %.0f, sbuf->issued %.0f, issued->sm0 sfull %.0f, sm0 sfull->pair %.0f, pair->arrive %.0f,"
+      " sm0 arrive->PV pfull %.0f, PV vfull(j)-> S sbuf(j+2) %.0f" % (
+      d(tr[:, 1], tr[:, 0]), d(tr[:, 2], tr[:, 1]), d(tr[:, 3], tr[:, 2]), d(tr[:, 4], tr[:, 3]), d(tr[:, 5], tr[:, 4]),
+      d(tr[:, 7], tr[:, 5]), np.median(tr[lo + 2:hi + 2, 1] - tr[lo:hi, 7])))
+print("median sm5: sfull->pair %.0f, pair->arrive %.0f" % (d(t2[:, 1], t2[:, 0]), d(t2[:, 2], t2[:, 1])))
