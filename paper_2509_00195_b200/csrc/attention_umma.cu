@@ -52,6 +52,10 @@ constexpr int kKSlot = kU * kTile;           // 32 KiB: K of a unit, [d half][pa
 constexpr int kVSlot = kU * kTile;           // 32 KiB: V of a unit, [page][d half][16 tokens][128 B]
 constexpr int kNK = 3;                       // K ring slots (released when S = Q K^T has completed)
 constexpr int kNV = 3;                       // V ring slots (released when O += P V has completed)
+#ifndef TTS_PF
+#define TTS_PF 0
+#endif
+constexpr int kPF = TTS_PF;                  // L2 prefetch distance of the producers (units)
 constexpr int kNM = 6;                       // unit metadata ring (>= kNK + kNSB: see the K producer)
 constexpr int kUH = kU / 2;                  // pages per softmax warp half
 constexpr int kThreads = 384;                // warps 0-7 softmax, 8 K producer, 9 V producer, 10 S issuer, 11 PV issuer
@@ -110,7 +114,7 @@ __device__ long long g_prof[512][12][16];
 #ifdef TTS_TRACE
 __device__ long long g_trace[1024][8];
 __device__ long long g_trace2[1024][8];
-__device__ long long g_cta[4096][4];  // per CTA of the last launch: globaltimer at start / loop end / exit, units | smid << 32
+__device__ long long g_cta[4096][4];  // per CTA of the last launch: globaltimer at start / after the plan wait / exit, units | smid << 32
 // per call (launch id % 32768): [0] first attention CTA start, [1] last attention CTA exit,
 // [2] first k_plan block start, [3] last k_plan block exit (globaltimer; min/max by atomics)
 __device__ unsigned long long g_lspan[32768][4];
@@ -164,6 +168,7 @@ struct UParams {
   int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
   int round_robin;            // beam b of a group -> lane quadrant b % 4 (else blocks of consecutive beams)
   int split_partial_round;    // a last partial round of tiles goes through stream-K (else whole if >= 3/4 full)
+  int sched;                  // phase-1 tiles: 0 rotated in blocks of n_groups, 1 plain round-robin, 2 none (stream-K only)
   int64_t num_pages;
   float scale_log2;
   int launch_id;              // call counter (TTS_TRACE launch spans only)
@@ -490,6 +495,7 @@ __global__ void __maxnreg__(kMaxRegs)
   // Programmatic dependent launch: this grid starts while k_plan (the call's
   // append + plan) runs; everything below reads what k_plan writes.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) TTS_CTA(1, gtimer());  // the plan (and every earlier call) is complete
   if (warp == 0) {
     // the schedule depends on the plan's counts only (k_plan writes empty
     // plans under a sticky error), so every CTA of the launch derives the same
@@ -530,6 +536,17 @@ __global__ void __maxnreg__(kMaxRegs)
   if (4 * (T - k1 * Cg) >= 3 * Cg && !p.split_partial_round) ++k1;
   else if (k1 > 0 && T > k1 * Cg) --k1;
   if (k1 > 0 && T > k1 * Cg && (int64_t)k1 * maxu + 1 > U / Cg) k1 = 0;
+  if (p.sched == 2) k1 = 0;
+  // Phase-1 tile of CTA c in round k: tile k C + c, rotated by k inside
+  // aligned blocks of ng CTAs in full rounds, so that the ng groups of a slab
+  // still run side by side (pages they share are read from HBM about once,
+  // L2) while every CTA meets every group position over the rounds (their
+  // costs differ systematically).
+  const bool rot = p.sched == 0;
+  auto p1tile = [&](int c, int k) {
+    const int blk = c / ng * ng;
+    return (rot && blk + ng <= Cg && (k + 1) * Cg <= T) ? k * Cg + blk + (c - blk + k) % ng : k * Cg + c;
+  };
   const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   const int64_t base2 = F(min(k1 * Cg, T));
   const int64_t U2 = U - base2;
@@ -543,7 +560,14 @@ __global__ void __maxnreg__(kMaxRegs)
   const int C2 = bal ? Cg : (int)min((int64_t)Cg, U2);
   auto f1 = [&](int cc) {  // phase-1 units of CTAs [0, cc)
     int64_t a = 0;
-    for (int k = 0; k < k1; ++k) a += F(min(cc + k * Cg, T)) - F(min(k * Cg, T));
+    const int cb = cc / ng * ng;  // whole blocks: the same tiles as without rotation
+    for (int k = 0; k < k1; ++k) {
+      a += F(min(cb + k * Cg, T)) - F(min(k * Cg, T));
+      for (int c = cb; c < cc; ++c) {
+        const int t = p1tile(c, k);
+        if (t < T) a += F(t + 1) - F(t);
+      }
+    }
     return a;
   };
   auto start2 = [&](int cc) {
@@ -574,7 +598,7 @@ __global__ void __maxnreg__(kMaxRegs)
   // piece idx of this CTA; pslot: partial-state slot (-1: phase 1, whole tile)
   auto piece = [&](int idx, int& gi, int& slab, int& j0, int& j1, int& pslot) {
     if (idx < n1) {
-      const int t = blockIdx.x + idx * Cg;
+      const int t = p1tile(blockIdx.x, idx);
       slab = t / ng;
       gi = t - slab * ng;
       j0 = 0;
@@ -611,19 +635,37 @@ __global__ void __maxnreg__(kMaxRegs)
       const int nit = __ldg(p.counts + gi);
       const int4* its = p.items + ((int64_t)g.req * p.maxB + g.beam0) * p.maxP;
       const int64_t layer_rows = ((int64_t)layer * p.num_pages) * p.Hkv;
+      // lanes [0, kU): page `lane` of the next unit; lanes [kU, 2 kU): page
+      // lane - kU of the unit kPF ahead, prefetched into L2 (more bytes in flight
+      // than the shared-memory ring holds)
+      const int pg = lane & (kU - 1);
       auto item = [&](int v) {
-        const int i = kU * v + lane;
-        return (lane < kU && v < j1 && i < nit) ? __ldg(its + i) : make_int4(-2, 0, 0, 0);
+        const int i = kU * v + pg;
+        return (lane < 2 * kU && v < j1 && i < nit) ? __ldg(its + i) : make_int4(-2, 0, 0, 0);
       };
-      int4 nx = item(j0);
+      auto prefetch = [&](const int4& m) {
+        if (kPF > 0 && lane >= kU && lane < 2 * kU && m.x >= 0) {
+          const int y = (int)((layer_rows + (int64_t)m.x * p.Hkv + kh) * kP);
+          if (is_k) {
+            tma2d_prefetch(&tmk, 0, y);
+            tma2d_prefetch(&tmk, 64, y);
+          } else {
+            tma3d_prefetch(&tmv, 0, y, 0);
+          }
+        }
+      };
+      if (kPF > 0)
+        for (int d = 0; d < kPF; ++d) prefetch(item(j0 + d));
+      int4 nx = item(lane < kU ? j0 : j0 + kPF);
       for (int v = j0; v < j1; ++v, ++js) {
         const int4 m = nx;
-        nx = item(v + 1);
+        nx = item(lane < kU ? v + 1 : v + 1 + kPF);
+        prefetch(m);
         PROF_MARK(2);
         bar_wait(b_e + 8 * slot, ph ^ 1u);
         PROF_MARK(0);
         if (lane == 0) TTS_TR2(js, is_k ? 3 : 4);
-        const bool has = m.x >= 0;
+        const bool has = lane < kU && m.x >= 0;
         const uint32_t np = __popc(__ballot_sync(0xffffffffu, has));
         const uint32_t fb = b_f + 8 * slot;
         if (is_k && lane < kU) meta[(js % kNM) * kU + lane] = m;
@@ -1066,7 +1108,6 @@ __global__ void __maxnreg__(kMaxRegs)
   }
 
   if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
-  if (threadIdx.x == 0) TTS_CTA(1, gtimer());
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
@@ -1078,7 +1119,7 @@ __global__ void __maxnreg__(kMaxRegs)
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     long long units = ub2 - ua2;
     for (int k = 0; k < n1; ++k) {
-      const int t = blockIdx.x + k * Cg, gi = t % ng;
+      const int t = p1tile(blockIdx.x, k), gi = t % ng;
       units += s_pre[gi + 1] - s_pre[gi];
     }
     TTS_CTA(3, units | ((long long)smid << 32));
@@ -1210,6 +1251,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.scale_log2 = scale * 1.4426950408889634f;
   p.round_robin = c->env_round_robin;
   p.split_partial_round = c->env_split_partial;
+  p.sched = c->env_sched;
   p.launch_id = (int)c->launches;
   UInline inl;  // host staging of the parameter block (copied by the launch)
   if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {

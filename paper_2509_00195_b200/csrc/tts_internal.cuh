@@ -115,6 +115,8 @@ struct Ctx {
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
   int env_round_robin = 0;    // TTS_ROUND_ROBIN=1: beam b of a group on lane quadrant b % 4
+  int env_sched = 2;          // TTS_SCHED: phase-1 tile assignment of k_tree_umma (0 rotated, 1 round-robin, 2 none:
+                              // every unit split evenly, measured fastest on C3)
   int env_split_partial = 0;  // TTS_SPLIT_PARTIAL=1: a partial last round of tiles goes through stream-K
   int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
   // multi-GPU (span.cu)
