@@ -859,7 +859,8 @@ def main():
                        "prompt": cfg.prompt, "steps_x_len": f"{cfg.n_steps}x{cfg.step_len or 'lognormal'}",
                        "beam_steps_per_rank_step": b.beam_steps,
                        "l2": (f"unique KV per call {unique_b / max(1, b.n_calls) / 1e6:.0f} MB vs 126 MB L2; "
-                              + (f"rotation over {len(greqs)} independent requests, {b.per_call} per call"
+                              + ("one request whose beams span the ranks" if span else
+                                 f"rotation over {len(greqs)} independent requests, {b.per_call} per call"
                                  if not b.batched else "batched requests")),
                        "parallelism": (f"beam-sharded x{ws} (one request's beams span the ranks; NCCL all-gather "
                                        "of scores + lineage migration per step)" if span else

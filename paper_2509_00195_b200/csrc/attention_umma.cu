@@ -536,7 +536,17 @@ __global__ void __maxnreg__(kMaxRegs)
   if (4 * (T - k1 * Cg) >= 3 * Cg && !p.split_partial_round) ++k1;
   else if (k1 > 0 && T > k1 * Cg) --k1;
   if (k1 > 0 && T > k1 * Cg && (int64_t)k1 * maxu + 1 > U / Cg) k1 = 0;
-  if (p.sched == 2) k1 = 0;
+  if (p.sched >= 2) k1 = 0;
+  // Unit order of the stream-K phase: slab-major (tile = slab * ng + group),
+  // or group-major (sched 3: every slab of group 0, then group 1, ...), which
+  // puts the ng groups of a slab on CTAs about C / ng apart at the same
+  // relative offset -- processed at the same time, so the pages they share
+  // hit L2 -- with the same exact unit balance.
+  const bool gmaj = p.sched == 3;
+  const int nslab = p.n_layers * p.Hkv;
+  auto U0 = [&](int gi, int slab) -> int64_t {  // first unit of tile (slab, gi) in the sequence
+    return gmaj ? (int64_t)nslab * s_pre[gi] + (int64_t)slab * (s_pre[gi + 1] - s_pre[gi]) : (int64_t)slab * S + s_pre[gi];
+  };
   // Phase-1 tile of CTA c in round k: tile k C + c, rotated by k inside
   // aligned blocks of ng CTAs in full rounds, so that the ng groups of a slab
   // still run side by side (pages they share are read from HBM about once,
@@ -577,6 +587,21 @@ __global__ void __maxnreg__(kMaxRegs)
   const int64_t ub2 = (int)blockIdx.x < C2 ? start2(blockIdx.x + 1) : 0;
   // the tile piece containing global unit u (phase 2): units [j0, j1) of tile (slab, gi)
   auto piece_at = [&](int64_t u, int& gi, int& slab, int& j0, int& j1) {
+    if (gmaj) {
+      int lo = 0, hi = ng;  // largest group with nslab * s_pre[gi] <= u
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)nslab * s_pre[mid] <= u) lo = mid;
+        else hi = mid;
+      }
+      gi = lo;
+      const int ug = s_pre[gi + 1] - s_pre[gi];
+      const int64_t rel = u - (int64_t)nslab * s_pre[gi];
+      slab = (int)(rel / ug);
+      j0 = (int)(rel - (int64_t)slab * ug);
+      j1 = (int)min((int64_t)ug, (int64_t)j0 + (ub2 - u));
+      return;
+    }
     slab = (int)(u / S);
     const int o = (int)(u - (int64_t)slab * S);
     int lo = 0, hi = ng;
@@ -595,7 +620,11 @@ __global__ void __maxnreg__(kMaxRegs)
     piece_at(u, gi, slab, j0, j1);
     u += j1 - j0;
   }
-  // piece idx of this CTA; pslot: partial-state slot (-1: phase 1, whole tile)
+  // piece idx of this CTA; pslot: partial-state slot (-1: phase 1, whole tile).
+  // Each warp walks its pieces in order: the phase-2 cursor (first unit of the
+  // last piece looked up, and its index) makes the next lookup O(1).
+  int64_t cur_u = ua2;
+  int cur_idx = n1;
   auto piece = [&](int idx, int& gi, int& slab, int& j0, int& j1, int& pslot) {
     if (idx < n1) {
       const int t = p1tile(blockIdx.x, idx);
@@ -606,13 +635,17 @@ __global__ void __maxnreg__(kMaxRegs)
       pslot = -1;
       return;
     }
-    int64_t u = ua2;
-    for (int q = idx - n1;; --q) {
-      piece_at(u, gi, slab, j0, j1);
-      if (q == 0) break;
-      u += j1 - j0;
+    if (idx < cur_idx) {
+      cur_idx = n1;
+      cur_u = ua2;
     }
-    pslot = 2 * blockIdx.x + (u == ua2 ? 0 : 1);
+    for (;;) {
+      piece_at(cur_u, gi, slab, j0, j1);
+      if (cur_idx == idx) break;
+      cur_u += j1 - j0;
+      ++cur_idx;
+    }
+    pslot = 2 * blockIdx.x + (cur_u == ua2 ? 0 : 1);
   };
 
   if (warp == 8 || warp == 9) {
@@ -806,6 +839,19 @@ __global__ void __maxnreg__(kMaxRegs)
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
+      if (pc + 1 < n_pieces) {
+        // the next piece's Q rows -> L2 now, so that its load after this
+        // piece's last unit does not wait for HBM
+        int gi2, slab2, j02, j12, ps2;
+        piece(pc + 1, gi2, slab2, j02, j12, ps2);
+        const GroupDesc g2 = group_of(gi2);
+        int bl2, hd2;
+        if (row_of(g2, r, bl2, hd2)) {
+          const __nv_bfloat16* q2 = p.q + ((((int64_t)(slab2 / p.Hkv) * p.n_call + g2.call_idx) * p.maxB + g2.beam0 + bl2) * p.Hq +
+                                           (slab2 % p.Hkv) * G + hd2) * kD + (warp >> 2) * 64;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(q2));
+        }
+      }
       const GroupDesc g = group_of(gi);
       int rbl = 0, rh = 0;
       const bool rvalid = row_of(g, r, rbl, rh);
@@ -1014,7 +1060,7 @@ __global__ void __maxnreg__(kMaxRegs)
                                  __uint_as_float(o[c2][4 * i + 2]), __uint_as_float(o[c2][4 * i + 3])));
           __threadfence();
           asm volatile("bar.sync 1, 256;" ::: "memory");
-          const int64_t T0 = F(slab * ng + gi);
+          const int64_t T0 = U0(gi, slab);
           auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
             if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
             int lo = 0, hi = C2;  // largest c with start2(c) <= x
