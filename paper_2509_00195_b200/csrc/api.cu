@@ -29,7 +29,7 @@ size_t workspace_bytes(const tts_config_t& c) {
   s += align_up(2 * rows * c.max_pages_per_beam * 16);  // attention plan items (double-buffered)
   s += align_up(2 * rows * 4);                          // plan counts
   s += align_up(umma_partial_bytes());                  // split tiles' partial states
-  s += align_up((size_t)c.num_layers * c.num_kv_heads * umma_max_groups() * 4);  // split-tile counters
+  s += align_up((size_t)2 * c.num_layers * c.num_kv_heads * umma_max_groups() * 4);  // split-tile counters
   s += align_up(1024 * 4);                          // global selection: gid-indexed scores
   s += align_up(1024 * 4);                          // global parent map
   s += (size_t)kUploadSlots * kUploadSlotBytes;     // upload mirror
@@ -168,7 +168,8 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   c->ws_partial = (float*)w;
   w += tts::align_up(tts::umma_partial_bytes());
   c->ws_tile_cnt = (int32_t*)w;
-  const size_t cnt_bytes = (size_t)cfg->num_layers * cfg->num_kv_heads * tts::umma_max_groups() * 4;
+  // (x2: pair mode counts the pieces of each rank's rows separately)
+  const size_t cnt_bytes = (size_t)2 * cfg->num_layers * cfg->num_kv_heads * tts::umma_max_groups() * 4;
   w += tts::align_up(cnt_bytes);
   c->ws_scores_all = (float*)w;
   w += tts::align_up(1024 * 4);
@@ -189,6 +190,7 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_ROUND_ROBIN")) c->env_round_robin = std::atoi(s) != 0;
   if (const char* s = std::getenv("TTS_SPLIT_PARTIAL")) c->env_split_partial = std::atoi(s) != 0;
   if (const char* s = std::getenv("TTS_SCHED")) c->env_sched = std::atoi(s);
+  if (const char* s = std::getenv("TTS_PAIR")) c->env_pair = std::atoi(s);
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;
@@ -395,6 +397,7 @@ static void plan_groups(tts_ctx_t c, int n_req, const int32_t* req_ids, const ui
 // host length mirror.  No side effect.
 struct AttnPlan {
   bool umma = false;
+  bool pair = false;    // tcgen05 path: 2-CTA clusters (groups of up to umma_pair_max_beams beams)
   int group_beams = 0;  // mma.sync path: beams per CTA group
   std::vector<tts::GroupDesc> groups;
   std::vector<int32_t> glens;  // tcgen05 path: per group beam, current length (0 = inactive)
@@ -424,8 +427,15 @@ static tts_status_t attn_prepare(tts_ctx_t c, int32_t layer_begin, int32_t layer
     // 59 us (the split pieces cost unequal time: the shared prefix at the head
     // of a tile keeps all four softmax warps busy, a private tail one).
     int maxb = tts::umma_max_beams(c);
+    // pair mode when every request of the call has more beams than one CTA's
+    // tile holds: a group of up to twice as many beams per 2-CTA cluster, so
+    // that the pages the two halves share are loaded once (TMA multicast)
+    const int pmax = c->env_pair ? tts::umma_pair_max_beams(c) : 0;
+    ap.pair = pmax > maxb && !c->env_group_beams;
+    for (int i = 0; ap.pair && i < n_req; ++i) ap.pair = c->n_beams[req_ids[i]] > maxb;
+    if (ap.pair) maxb = pmax;
     if (c->env_group_beams) maxb = std::max(1, std::min(maxb, c->env_group_beams));
-    const int64_t want = (3ll * c->num_sms + 3) / 4;
+    const int64_t want = (3ll * (ap.pair ? c->num_sms / 2 : c->num_sms) + 3) / 4;
     auto group_size = [&](int cap) {
       int gb = 1;
       for (int i = 0; i < n_req; ++i) {
@@ -481,7 +491,7 @@ static tts_status_t attn_launch(tts_ctx_t c, const AttnPlan& ap, int32_t layer_b
                                         (int)ap.glens.size(), layer_begin, n_layers, n_req,
                                         (const __nv_bfloat16*)q, scale, out,
                                         append ? (const __nv_bfloat16*)k_new : nullptr,
-                                        append ? (const __nv_bfloat16*)v_new : nullptr, st));
+                                        append ? (const __nv_bfloat16*)v_new : nullptr, st, ap.pair));
     if (e1) TTS_CUDA(cudaEventRecord(e1, st));
     return TTS_OK;
   }

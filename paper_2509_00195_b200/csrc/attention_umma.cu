@@ -385,7 +385,11 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
 // the per-group unit counts (prefix in smem).
 // kPoly: exponentials on the FMA/ALU pipes (ex2_poly2) instead of MUFU: 1 = every other pair, 2 = all
 // instead of MUFU.
-template <int kPoly>
+// kPair: a cluster of two CTAs per tile of a group of up to 32 beams (each
+// CTA the rows of half the beams): every K/V page of a unit is loaded once
+// for both (TMA multicast, each CTA issuing half of the pages), so pages the
+// two halves share are not fetched twice.
+template <int kPoly, bool kPair>
 __global__ void __maxnreg__(kMaxRegs)
     k_tree_umma(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv, UParams p,
                 const __grid_constant__ UInline inl) {
@@ -409,19 +413,22 @@ __global__ void __maxnreg__(kMaxRegs)
                  b_pv = b_pfull + 8 * kNSB, b_qready = b_pv + 8 * kNSB, b_ofree = b_qready + 8, b_qtaken = b_ofree + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // pair mode: this CTA's rank in its cluster, and the scheduling index (the pair)
+  const int rank = kPair ? (int)cluster_ctarank() : 0;
+  const int cta = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const uint16_t kBoth = 3;
   if (threadIdx.x == 0) TTS_TR(1023, 0);  // CTA start
   if (threadIdx.x == 0) TTS_CTA(0, gtimer());
   if (threadIdx.x == 0) TTS_SPAN(p.launch_id, 0, gtimer(), atomicMin);
-  // the next call's k_plan may start as soon as every CTA of this grid runs
-  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x == 0) {
+    // (pair mode: a slot is free once both CTAs' MMAs have read it)
     for (int i = 0; i < kNK; ++i) {
       bar_init(b_kfull + 8 * i, 1);
-      bar_init(b_kempty + 8 * i, 1);
+      bar_init(b_kempty + 8 * i, kPair ? 2 : 1);
     }
     for (int i = 0; i < kNV; ++i) {
       bar_init(b_vfull + 8 * i, 1);
-      bar_init(b_vempty + 8 * i, 1);
+      bar_init(b_vempty + 8 * i, kPair ? 2 : 1);
     }
     for (int i = 0; i < kNSB; ++i) {
       bar_init(b_sfull + 8 * i, 1);
@@ -440,6 +447,7 @@ __global__ void __maxnreg__(kMaxRegs)
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the partner's barriers exist before any multicast reaches them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_o = tmem, t_s = tmem + kTS;
@@ -447,7 +455,7 @@ __global__ void __maxnreg__(kMaxRegs)
   const int G = p.G;
   const int ng = p.n_groups;
   const int T = p.n_layers * p.Hkv * ng;
-  const int Cg = gridDim.x;
+  const int Cg = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;  // scheduling units (pairs)
   auto group_of = [&](int gi) { return p.groups ? p.groups[gi] : inl.g[gi]; };
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const int r = (warp & 3) * 32 + lane;  // softmax warps: the TMEM lane (tile row) of this thread
@@ -457,12 +465,32 @@ __global__ void __maxnreg__(kMaxRegs)
   // by the warps holding one of its member beams, so spreading the beams
   // evenly spreads the softmax work of private pages over all four warps.
   const bool kRoundRobin = p.round_robin != 0;
+  // (pair mode: rank 0 holds beams [0, ceil(nb/2)), rank 1 the rest)
   auto row_of = [&](const GroupDesc& g, int row, int& beam, int& head) {
-    const int bpw = (g.nbeams + 3) >> 2;
+    const int nbh = kPair ? (g.nbeams + 1) >> 1 : g.nbeams;
+    const int boff = rank * nbh, nbl = kPair && rank ? g.nbeams - nbh : nbh;
+    const int bpw = (nbl + 3) >> 2;
     const int l = row & 31, bw = l / G;
-    beam = kRoundRobin ? bw * 4 + (row >> 5) : (row >> 5) * bpw + bw;
+    const int lb = kRoundRobin ? bw * 4 + (row >> 5) : (row >> 5) * bpw + bw;
+    beam = boff + lb;
     head = l - bw * G;
-    return bw < bpw && beam < g.nbeams && ((g.active >> beam) & 1u);
+    return bw < bpw && lb < nbl && ((g.active >> beam) & 1u);
+  };
+  // pair mode: the unit's pages read by none of this CTA's beams need no MMA
+  // here (the partner's private pages); both issuing warps take the same
+  // decision from the unit metadata
+  auto cta_reads = [&](const GroupDesc& g, const int4* mrow) {
+    if (!kPair) return true;
+    const int nbh = (g.nbeams + 1) >> 1;
+    const int nbl = rank ? g.nbeams - nbh : nbh;
+    const uint32_t mine = (((1u << nbl) - 1u) << (rank * nbh)) & g.active;
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int4 m = mrow[k];
+      any |= m.x >= 0 ? ((uint32_t)m.y & mine) : 0u;
+    }
+    return any != 0u;
   };
   // Q rows of a piece -> TMEM (the A operand of S = Q K^T): lane = row, column = d pair
   auto load_q = [&](int gi, int slab) {
@@ -496,6 +524,10 @@ __global__ void __maxnreg__(kMaxRegs)
   // append + plan) runs; everything below reads what k_plan writes.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) TTS_CTA(1, gtimer());  // the plan (and every earlier call) is complete
+  // the next call's k_plan may start once every CTA of this grid is past the
+  // wait: the previous call's attention kernel has then exited, so the plan
+  // buffer that k_plan overwrites (parity of the previous call) is free
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   if (warp == 0) {
     // the schedule depends on the plan's counts only (k_plan writes empty
     // plans under a sticky error), so every CTA of the launch derives the same
@@ -557,7 +589,7 @@ __global__ void __maxnreg__(kMaxRegs)
     const int blk = c / ng * ng;
     return (rot && blk + ng <= Cg && (k + 1) * Cg <= T) ? k * Cg + blk + (c - blk + k) % ng : k * Cg + c;
   };
-  const int n1 = (int)blockIdx.x < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
+  const int n1 = cta < T - (k1 - 1) * Cg ? k1 : k1 - 1;  // this CTA's whole tiles
   const int64_t base2 = F(min(k1 * Cg, T));
   const int64_t U2 = U - base2;
   // phase-2 CTAs: every one gets >= 1 unit (a split tile's pieces are then
@@ -583,8 +615,8 @@ __global__ void __maxnreg__(kMaxRegs)
   auto start2 = [&](int cc) {
     return bal ? base2 + (int64_t)cc * U / Cg - f1(cc) : base2 + (int64_t)cc * U2 / C2;
   };
-  const int64_t ua2 = (int)blockIdx.x < C2 ? start2(blockIdx.x) : 0;
-  const int64_t ub2 = (int)blockIdx.x < C2 ? start2(blockIdx.x + 1) : 0;
+  const int64_t ua2 = cta < C2 ? start2(cta) : 0;
+  const int64_t ub2 = cta < C2 ? start2(cta + 1) : 0;
   // the tile piece containing global unit u (phase 2): units [j0, j1) of tile (slab, gi)
   auto piece_at = [&](int64_t u, int& gi, int& slab, int& j0, int& j1) {
     if (gmaj) {
@@ -627,7 +659,7 @@ __global__ void __maxnreg__(kMaxRegs)
   int cur_idx = n1;
   auto piece = [&](int idx, int& gi, int& slab, int& j0, int& j1, int& pslot) {
     if (idx < n1) {
-      const int t = p1tile(blockIdx.x, idx);
+      const int t = p1tile(cta, idx);
       slab = t / ng;
       gi = t - slab * ng;
       j0 = 0;
@@ -698,8 +730,11 @@ __global__ void __maxnreg__(kMaxRegs)
         bar_wait(b_e + 8 * slot, ph ^ 1u);
         PROF_MARK(0);
         if (lane == 0) TTS_TR2(js, is_k ? 3 : 4);
-        const bool has = lane < kU && m.x >= 0;
-        const uint32_t np = __popc(__ballot_sync(0xffffffffu, has));
+        // pair mode: every page lands in both CTAs; this CTA issues pages
+        // [kU/2 rank, kU/2 (rank + 1)), the partner the others
+        const bool present = lane < kU && m.x >= 0;
+        const bool has = present && (!kPair || (lane / (kU / 2)) == rank);
+        const uint32_t np = __popc(__ballot_sync(0xffffffffu, present));
         const uint32_t fb = b_f + 8 * slot;
         if (is_k && lane < kU) meta[(js % kNM) * kU + lane] = m;
         if (lane == 0) bar_expect(fb, np * (uint32_t)kTile);
@@ -709,11 +744,17 @@ __global__ void __maxnreg__(kMaxRegs)
           if (is_k) {
             // K: [d half][page][16 tokens][128 B] (one 128-row K-major operand over the unit)
             const uint32_t sb = base + kOffK + slot * kKSlot + lane * (kTile / 2);
-            tma2d(sb, &tmk, 0, y, fb);
-            tma2d(sb + kU * (kTile / 2), &tmk, 64, y, fb);
+            if (kPair) {
+              tma2d_mc(sb, &tmk, 0, y, fb, kBoth);
+              tma2d_mc(sb + kU * (kTile / 2), &tmk, 64, y, fb, kBoth);
+            } else {
+              tma2d(sb, &tmk, 0, y, fb);
+              tma2d(sb + kU * (kTile / 2), &tmk, 64, y, fb);
+            }
           } else {
             // V: [page][d half][16][128 B] (3D box)
-            tma3d(base + kOffV + slot * kVSlot + lane * kTile, &tmv, 0, y, 0, fb);
+            if (kPair) tma3d_mc(base + kOffV + slot * kVSlot + lane * kTile, &tmv, 0, y, 0, fb, kBoth);
+            else tma3d(base + kOffV + slot * kVSlot + lane * kTile, &tmv, 0, y, 0, fb);
           }
         }
         __syncwarp();
@@ -739,6 +780,7 @@ __global__ void __maxnreg__(kMaxRegs)
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
+      const GroupDesc g = group_of(gi);
       PROF_MARK(2);
       bar_wait(b_qready, pc & 1);  // this piece's Q in TMEM
       PROF_MARK(3);
@@ -760,13 +802,15 @@ __global__ void __maxnreg__(kMaxRegs)
         // each; an absent page leaves its 16 columns undefined: masked)
         const uint32_t sd = t_s + (js % kNSB) * kSCols;
         const uint64_t dk = dk0 + (uint64_t)((slot * kKSlot) >> 4);
+        const bool run = cta_reads(g, meta + (js % kNM) * kU);
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
-            mma_ss(sd, dq0 + (uint64_t)(((ks >> 2) * (kRows * 128) + (ks & 3) * 32) >> 4),
+            if (run) mma_ss(sd, dq0 + (uint64_t)(((ks >> 2) * (kRows * 128) + (ks & 3) * 32) >> 4),
                    dk + (uint64_t)(((ks >> 2) * (kKSlot / 2) + (ks & 3) * 32) >> 4), id_s, ks > 0);
           tc_commit(b_sfull + 8 * (js % kNSB));
-          tc_commit(b_kempty + 8 * slot);
+          if (kPair) tc_commit_mc(b_kempty + 8 * slot, kBoth);
+          else tc_commit(b_kempty + 8 * slot);
         }
         __syncwarp();
         if (lane == 0) TTS_TR(js, 2);
@@ -784,6 +828,8 @@ __global__ void __maxnreg__(kMaxRegs)
     for (int pc = 0; pc < n_pieces; ++pc) {
       int gi, slab, j0, j1, pslot;
       piece(pc, gi, slab, j0, j1, pslot);
+      const GroupDesc g = group_of(gi);
+      uint32_t acc = 0;  // O written by an earlier PV of this piece
       for (int j = j0; j < j1; ++j, ++js) {
         const int slot = js % kNV;
         PROF_MARK(3);
@@ -800,16 +846,20 @@ __global__ void __maxnreg__(kMaxRegs)
         const uint32_t pa = t_s + (js % kNSB) * kSCols;
         const int4* mrow = meta + (js % kNM) * kU;
         const bool e = elect_one();
-        uint32_t acc = j != j0;
+        // (pair mode: a unit this CTA does not read is skipped -- its P is
+        // zero -- unless it is the piece's last and O was never written: then
+        // O = 0 . V initialises it)
+        const bool run = cta_reads(g, mrow) || (j + 1 == j1 && !acc);
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
-          if (mrow[k].x < 0) continue;
+          if (mrow[k].x < 0 || !run) continue;
           const uint64_t dv = dv0 + (uint64_t)((slot * kVSlot + k * kTile) >> 4);
           if (e) mma_ts(t_o, pa + k * (kP / 2), dv, id_pv, acc);
           acc = 1;
         }
         if (e) {
-          tc_commit(b_vempty + 8 * slot);
+          if (kPair) tc_commit_mc(b_vempty + 8 * slot, kBoth);
+          else tc_commit(b_vempty + 8 * slot);
           tc_commit(b_pv + 8 * (js % kNSB));
         }
         __syncwarp();
@@ -1072,7 +1122,7 @@ __global__ void __maxnreg__(kMaxRegs)
             return lo;
           };
           const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
-          const int tile = slab * ng + gi;
+          const int tile = (slab * ng + gi) * (kPair ? 2 : 1) + rank;  // (pair mode: each rank merges its own rows)
           if (threadIdx.x == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
           asm volatile("bar.sync 1, 256;" ::: "memory");
           PROF_MARK(10);
@@ -1080,8 +1130,9 @@ __global__ void __maxnreg__(kMaxRegs)
             __threadfence();
             const int np = c_last - c_first + 1;
             // piece k's slot: only the first CTA's range can start before the tile
-            const int slot0 = 2 * c_first + (start2(c_first) >= T0 ? 0 : 1);
-            auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : 2 * (c_first + k)) * kPartFloats; };
+            auto cta_slot = [&](int c) { return 2 * (kPair ? 2 * c + rank : c); };  // first partial slot of CTA c's rank
+            const int slot0 = cta_slot(c_first) + (start2(c_first) >= T0 ? 0 : 1);
+            auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : cta_slot(c_first + k)) * kPartFloats; };
             // latency-bound (L2 round trips under full HBM load): every batch of
             // loads is issued before any is consumed
             float M = -INFINITY, L = 0.f;
@@ -1156,6 +1207,9 @@ __global__ void __maxnreg__(kMaxRegs)
   if (threadIdx.x == 0) TTS_TR(1023, 2);  // unit loop done
   tc_fence_before();
   __syncthreads();
+  // pair mode: the partner's last multicast loads / commits target this CTA's
+  // shared memory: neither exits before both are done
+  if (kPair) cluster_sync();
   if (threadIdx.x == 0) TTS_TR(1023, 3);  // epilogue / merge done
   if (threadIdx.x == 0) TTS_CTA(2, gtimer());
   if (threadIdx.x == 0) TTS_SPAN(p.launch_id, 1, gtimer(), atomicMax);
@@ -1165,7 +1219,7 @@ __global__ void __maxnreg__(kMaxRegs)
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     long long units = ub2 - ua2;
     for (int k = 0; k < n1; ++k) {
-      const int t = p1tile(blockIdx.x, k), gi = t % ng;
+      const int t = p1tile(cta, k), gi = t % ng;
       units += s_pre[gi + 1] - s_pre[gi];
     }
     TTS_CTA(3, units | ((long long)smid << 32));
@@ -1214,18 +1268,42 @@ bool umma_supported(const Ctx* c) {
          c->umma_ok;
 }
 
-// Per device context: the kernel attributes, and the residency argument the
-// plan's double buffer relies on.  The grid is exactly one CTA per SM and at
-// most one fits per SM (static_assert on the shared memory above), so all CTAs
-// of call N+1 being resident implies call N's attention kernel has exited --
-// and call N+2's k_plan (PDL-released by call N+1's CTAs) can only then
-// overwrite the plan buffer call N read.  A device with more SMs than the
-// partial-state slots cover uses the mma.sync path.
+// Per device context: the kernel attributes (single-CTA and pair kernels) and
+// the number of co-resident 2-CTA clusters.  The plan's double buffer needs no
+// residency argument: call N+1's k_plan is released only once every CTA of
+// call N's attention kernel is past its plan wait, i.e. after call N-1's
+// attention kernel (the reader of the buffer k_plan N+1 overwrites) exited.
+// A device with more SMs than the partial-state slots cover uses the mma.sync
+// path.
 cudaError_t umma_prepare(Ctx* c) {
   c->umma_ok = false;
+  c->umma_pair_ctas = 0;
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
   if (c->cfg.head_dim != kD || c->cfg.page_size != kP || G < 4 || G > 16) return cudaSuccess;
-  for (auto k : {k_tree_umma<0>, k_tree_umma<1>, k_tree_umma<2>}) {
+  for (auto k : {k_tree_umma<0, true>, k_tree_umma<1, true>, k_tree_umma<2, true>}) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(2 * (c->num_sms / 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
+    if (e != cudaSuccess) {  // no pair mode on this device (the single-CTA kernel still works)
+      (void)cudaGetLastError();
+      ncl = 0;
+    }
+    const int ctas = std::min(2 * ncl, 2 * (c->num_sms / 2));
+    c->umma_pair_ctas = c->umma_pair_ctas ? std::min(c->umma_pair_ctas, ctas) : ctas;
+  }
+  for (auto k : {k_tree_umma<0, false>, k_tree_umma<1, false>, k_tree_umma<2, false>}) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
     // the whole shared-memory carveout
@@ -1241,6 +1319,11 @@ cudaError_t umma_prepare(Ctx* c) {
   return cudaSuccess;
 }
 
+int umma_pair_max_beams(const Ctx* c) {
+  // two CTAs of up to umma_max_beams beams each; the plan's member masks hold 32 beams
+  return c->umma_pair_ctas >= 2 ? std::min(32, 2 * umma_max_beams(c)) : 0;
+}
+
 int umma_max_beams(const Ctx* c) {
   // four softmax warps, each holding whole beams (G lanes per beam)
   const int G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
@@ -1250,7 +1333,7 @@ int umma_max_beams(const Ctx* c) {
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
                                   int n_lens, int layer_begin, int n_layers, int n_call,
                                   const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
-                                  const __nv_bfloat16* v_new, cudaStream_t st) {
+                                  const __nv_bfloat16* v_new, cudaStream_t st, bool pair) {
   PlanParams pp;
   pp.lens = c->buf.seq_lens;
   pp.tables = c->buf.block_tables;
@@ -1313,7 +1396,8 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     pp.glens = (const int32_t*)dl;
   }
   // measured 2% slower on C2/C3 (the softmax is latency-, not MUFU-bound): off unless TTS_POLY=1
-  auto kern = c->env_poly == 2 ? k_tree_umma<2> : c->env_poly ? k_tree_umma<1> : k_tree_umma<0>;
+  auto kern = pair ? (c->env_poly == 2 ? k_tree_umma<2, true> : c->env_poly ? k_tree_umma<1, true> : k_tree_umma<0, true>)
+                   : (c->env_poly == 2 ? k_tree_umma<2, false> : c->env_poly ? k_tree_umma<1, false> : k_tree_umma<0, false>);
   const bool no_pdl = c->env_no_pdl;
   cudaLaunchAttribute pdl;
   // each kernel may start while its predecessor on the stream runs; both wait
@@ -1332,12 +1416,20 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c->num_sms);  // persistent: one CTA per SM (<= kMaxCtas, umma_prepare)
+  // persistent: one CTA per SM (<= kMaxCtas, umma_prepare); pair mode: the
+  // co-resident 2-CTA clusters
+  cfg.gridDim = dim3(pair ? c->umma_pair_ctas : c->num_sms);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = st;
-  cfg.attrs = &pdl;
-  cfg.numAttrs = no_pdl ? 0 : 1;
+  cudaLaunchAttribute at[2];
+  at[0] = pdl;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = pair ? 2 : 1;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = no_pdl ? at + 1 : at;
+  cfg.numAttrs = no_pdl ? 1 : 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, c->tmap_k, c->tmap3_v, p, inl);
   c->launches++;
   return e;

@@ -115,10 +115,12 @@ struct Ctx {
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
   int env_round_robin = 0;    // TTS_ROUND_ROBIN=1: beam b of a group on lane quadrant b % 4
+  int env_pair = 0;           // TTS_PAIR=1: 2-CTA clusters for groups of > umma_max_beams beams (measured slower)
   int env_sched = 2;          // TTS_SCHED: phase-1 tile assignment of k_tree_umma (0 rotated, 1 round-robin, 2 none:
                               // every unit split evenly, measured fastest on C3)
   int env_split_partial = 0;  // TTS_SPLIT_PARTIAL=1: a partial last round of tiles goes through stream-K
   int umma_occupancy = 0;     // resident k_tree_umma CTAs per SM found by umma_prepare
+  int umma_pair_ctas = 0;     // pair mode: CTAs of the co-resident 2-CTA clusters (0: pair mode unavailable)
   // multi-GPU (span.cu)
   Comm* comm = nullptr;
   std::map<int, Span> spans;
@@ -211,6 +213,8 @@ int umma_max_groups();
 cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_groups, const int32_t* lens_h,
                                   int n_lens, int layer_begin, int n_layers, int n_call,
                                   const __nv_bfloat16* q, float scale, float* out, const __nv_bfloat16* k_new,
-                                  const __nv_bfloat16* v_new, cudaStream_t s);
+                                  const __nv_bfloat16* v_new, cudaStream_t s, bool pair);
+// pair mode: groups of up to this many beams, one 2-CTA cluster per tile (0: unavailable)
+int umma_pair_max_beams(const Ctx* c);
 
 }  // namespace tts

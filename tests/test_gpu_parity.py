@@ -169,3 +169,18 @@ def test_selection_dynamic_c1_tie_scores():
     cfg = workload.C1.with_(n_steps=4)
     table = {0: [0.9, 0.1, 0.5, 0.5], 1: [0.5, 0.75, 0.75, 0.75], 2: [0.8, 0.2, 0.0, float("nan")]}
     run_parity(cfg, all_beams(cfg, 5), scores_fn=lambda r, s: table[s], policy=(2, 2))
+
+
+@pytest.mark.parametrize("name", ["C3-reduced", "C4-reduced"])
+def test_pair_mode(name, monkeypatch):
+    # TTS_PAIR=1: groups of up to 32 beams on 2-CTA clusters (TMA multicast of
+    # every page to both CTAs, each the rows of half the beams; units no row of
+    # a CTA reads are skipped there) -- same parity bar as the default path
+    monkeypatch.setenv("TTS_PAIR", "1")
+    if name == "C3-reduced":
+        cfg = workload.C3.with_(n_steps=3, L=2)
+        pts = _sample_points(cfg, [0, 17, 31, 40, 63], [0, 1])
+    else:
+        cfg = workload.C4.with_(R=3, n_steps=3, L=2)
+        pts = _sample_points(cfg, [0, 31, 100, 255], [0, 1])
+    run_parity(cfg, pts, check_refs=False)
