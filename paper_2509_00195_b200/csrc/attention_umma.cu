@@ -802,7 +802,13 @@ __global__ void __maxnreg__(kMaxRegs)
         // each; an absent page leaves its 16 columns undefined: masked)
         const uint32_t sd = t_s + (js % kNSB) * kSCols;
         const uint64_t dk = dk0 + (uint64_t)((slot * kKSlot) >> 4);
+        // (timing experiments only, outputs garbage: -DTTS_NOMMA_S drops S = Q K^T,
+        // -DTTS_MEMONLY every MMA and the softmax work -- DESIGN.md section 7)
+#if defined(TTS_NOMMA_S) || defined(TTS_MEMONLY)
+        const bool run = false;
+#else
         const bool run = cta_reads(g, meta + (js % kNM) * kU);
+#endif
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks)
@@ -849,7 +855,11 @@ __global__ void __maxnreg__(kMaxRegs)
         // (pair mode: a unit this CTA does not read is skipped -- its P is
         // zero -- unless it is the piece's last and O was never written: then
         // O = 0 . V initialises it)
+#if defined(TTS_NOMMA_PV) || defined(TTS_MEMONLY)  // (timing experiments only)
+        const bool run = j + 1 == j1 && !acc;
+#else
         const bool run = cta_reads(g, mrow) || (j + 1 == j1 && !acc);
+#endif
 #pragma unroll
         for (int k = 0; k < kU; ++k) {
           if (mrow[k].x < 0 || !run) continue;
@@ -926,7 +936,11 @@ __global__ void __maxnreg__(kMaxRegs)
           const int4 mt = mrow[k];
           lm |= (mt.x >= 0 && rvalid && ((((uint32_t)mt.y) >> rbl) & 1u)) ? 1u << k : 0u;
         }
+#ifdef TTS_MEMONLY  // (timing experiment only: no softmax work)
+        const uint32_t wmask = 0u * __reduce_or_sync(0xffffffffu, lm);
+#else
         const uint32_t wmask = __reduce_or_sync(0xffffffffu, lm);
+#endif
         uint32_t sr[kUH / 2][32];
         float mx = -INFINITY;
         if (wmask) {
