@@ -191,6 +191,7 @@ tts_status_t tts_create(const tts_config_t* cfg, const tts_buffers_t* bufs, int 
   if (const char* s = std::getenv("TTS_SPLIT_PARTIAL")) c->env_split_partial = std::atoi(s) != 0;
   if (const char* s = std::getenv("TTS_SCHED")) c->env_sched = std::atoi(s);
   if (const char* s = std::getenv("TTS_PAIR")) c->env_pair = std::atoi(s);
+  if (const char* s = std::getenv("TTS_L2HINT")) c->env_l2hint = std::atoi(s);
   if (!tts::make_tensor_maps(c)) {
     tts_destroy(c);
     return TTS_ERR_CUDA;

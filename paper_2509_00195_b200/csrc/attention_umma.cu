@@ -168,6 +168,7 @@ struct UParams {
   int layer_begin, n_layers, n_call, n_groups, Hq, Hkv, G, maxB, maxP;
   int round_robin;            // beam b of a group -> lane quadrant b % 4 (else blocks of consecutive beams)
   int split_partial_round;    // a last partial round of tiles goes through stream-K (else whole if >= 3/4 full)
+  int l2hint;                 // 1: pages held outside the group loaded L2::evict_last, the rest evict_first
   int sched;                  // phase-1 tiles: 0 rotated in blocks of n_groups, 1 plain round-robin, 2 none (stream-K only)
   int64_t num_pages;
   float scale_log2;
@@ -196,6 +197,7 @@ struct UInline {
 // beam's last page (V -> the pool's fp16); a fresh page's slots 1..P-1 zeroed.
 struct PlanParams {
   int32_t* lens;
+  const int32_t* refcounts;  // item.w = 1: the page is also held by beams outside the group
   const int32_t* tables;
   const GroupDesc* groups;  // device copies when the call does not fit the parameter block, else null
   const int32_t* glens;
@@ -353,7 +355,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
       const int t = entry(b);
       if (t >= 0) {
         if (t != last) {
-          if (last >= 0) out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+          if (last >= 0)
+            out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), __ldg(p.refcounts + last) > __popc(mem));
           last = t;
           mem = 1u << b;
           s0 = b;
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
         }
       }
     }
-    if (last >= 0) out[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), i);
+    if (last >= 0) out[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), __ldg(p.refcounts + last) > __popc(mem));
     base += tot;
     __syncthreads();
   }
@@ -689,6 +692,7 @@ __global__ void __maxnreg__(kMaxRegs)
     // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
     PROF_DECL;
     const int nslot = is_k ? kNK : kNV;
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     const uint32_t b_f = is_k ? b_kfull : b_vfull, b_e = is_k ? b_kempty : b_vempty;
     int slot = 0, js = 0;
     uint32_t ph = 0;
@@ -739,7 +743,19 @@ __global__ void __maxnreg__(kMaxRegs)
         if (is_k && lane < kU) meta[(js % kNM) * kU + lane] = m;
         if (lane == 0) bar_expect(fb, np * (uint32_t)kTile);
         __syncwarp();
-        if (has) {
+        if (has && p.l2hint && !kPair) {
+          // pages other groups also read stay in L2 for them; the group's own
+          // pages are streamed through
+          const uint64_t pol = m.w ? pol_keep : pol_stream;
+          const int y = (int)((layer_rows + (int64_t)m.x * p.Hkv + kh) * kP);
+          if (is_k) {
+            const uint32_t sb = base + kOffK + slot * kKSlot + lane * (kTile / 2);
+            tma2d_hint(sb, &tmk, 0, y, fb, pol);
+            tma2d_hint(sb + kU * (kTile / 2), &tmk, 64, y, fb, pol);
+          } else {
+            tma3d_hint(base + kOffV + slot * kVSlot + lane * kTile, &tmv, 0, y, 0, fb, pol);
+          }
+        } else if (has) {
           const int y = (int)((layer_rows + (int64_t)m.x * p.Hkv + kh) * kP);
           if (is_k) {
             // K: [d half][page][16 tokens][128 B] (one 128-row K-major operand over the unit)
@@ -1350,6 +1366,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
                                   const __nv_bfloat16* v_new, cudaStream_t st, bool pair) {
   PlanParams pp;
   pp.lens = c->buf.seq_lens;
+  pp.refcounts = c->buf.refcounts;
   pp.tables = c->buf.block_tables;
   pp.groups = nullptr;
   pp.glens = nullptr;
@@ -1395,6 +1412,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
   p.round_robin = c->env_round_robin;
   p.split_partial_round = c->env_split_partial;
   p.sched = c->env_sched;
+  p.l2hint = c->env_l2hint;
   p.launch_id = (int)c->launches;
   UInline inl;  // host staging of the parameter block (copied by the launch)
   if (n_groups <= kInlineGroups && n_lens <= kInlineLens) {

@@ -64,6 +64,33 @@ __device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* m, int x,
       : "memory");
 }
 
+// TMA loads with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma2d_hint(uint32_t dst, const CUtensorMap* m, int x, int y, uint32_t b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(b), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d_hint(uint32_t dst, const CUtensorMap* m, int x, int y, int z, uint32_t b,
+                                           uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(b), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // L2 prefetch of a tensor-map box (no shared memory, no completion)
 __device__ __forceinline__ void tma2d_prefetch(const CUtensorMap* m, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
