@@ -33,6 +33,7 @@
 // Three S/P buffers in TMEM keep three units between S = Q K^T and O += P V.
 // Each distinct page is fetched once per tile and multiplied against all its
 // rows: every GQA head and every beam of the tile that references it.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -87,6 +88,23 @@ static_assert(2 * (kSmemBytes + 1024) > 228 * 1024, "at most one CTA per SM (pla
 static_assert(kOffMeta % 16 == 0 && kOffBar % 8 == 0 && kOffXm % 16 == 0 && kOffQ % 1024 == 0, "shared-memory alignment");
 static_assert(kNM >= kNK + kNSB, "metadata ring reuse distance");
 static_assert(kOffV % 1024 == 0 && kKSlot % 1024 == 0, "SWIZZLE_128B atoms");
+
+// Device-side bounds checks of the schedule's indices (compute-sanitizer is not
+// available on the GPU pool): -DTTS_CHECK builds trap on a violation.
+#ifdef TTS_CHECK
+#define TTS_ASSERT(c)                                                                      \
+  do {                                                                                     \
+    if (!(c)) {                                                                            \
+      printf("TTS_ASSERT %s failed (line %d, block %d, thread %d)\n", #c, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                            \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define TTS_ASSERT(c) \
+  do {                \
+  } while (0)
+#endif
 
 #ifdef TTS_PROF
 // per CTA (last launch) x warp: accumulated cycles [0..5] + counters (tools/prof.py)
@@ -545,6 +563,7 @@ __global__ void __maxnreg__(kMaxRegs)
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
+      TTS_ASSERT(p.n_groups <= kMaxGroups && (int)blockIdx.x < kMaxCtas);
       if (i < p.n_groups) s_pre[i + 1] = run + x;
       run += __shfl_sync(0xffffffffu, x, 31);
     }
@@ -681,6 +700,8 @@ __global__ void __maxnreg__(kMaxRegs)
       ++cur_idx;
     }
     pslot = 2 * blockIdx.x + (cur_u == ua2 ? 0 : 1);
+    TTS_ASSERT(gi >= 0 && gi < ng && slab >= 0 && slab < p.n_layers * p.Hkv && 0 <= j0 && j0 <= j1 &&
+               j1 <= s_pre[gi + 1] - s_pre[gi]);
   };
 
   if (warp == 8 || warp == 9) {
@@ -1125,6 +1146,7 @@ __global__ void __maxnreg__(kMaxRegs)
           // CTA's first phase-2 piece, 2c + 1 for its last); O chunk-major ([32
           // chunks of 4 floats][128 rows]) so that a warp's accesses coalesce.
           // The last piece to finish merges.
+          TTS_ASSERT(pslot >= 0 && pslot < 2 * kMaxCtas);
           float* part = p.partial + (size_t)pslot * kPartFloats;
           if (hh == 0) {
             part[r] = m_ref;
@@ -1153,6 +1175,7 @@ __global__ void __maxnreg__(kMaxRegs)
           };
           const int c_first = cta_of(T0), c_last = cta_of(T0 + tu - 1);
           const int tile = (slab * ng + gi) * (kPair ? 2 : 1) + rank;  // (pair mode: each rank merges its own rows)
+          TTS_ASSERT(tile >= 0 && tile < 2 * p.n_layers * p.Hkv * kMaxGroups && c_first <= cta && cta <= c_last);
           if (threadIdx.x == 0) s_info[0] = atomicAdd(p.tile_cnt + tile, 1) == c_last - c_first;
           asm volatile("bar.sync 1, 256;" ::: "memory");
           PROF_MARK(10);
@@ -1162,6 +1185,7 @@ __global__ void __maxnreg__(kMaxRegs)
             // piece k's slot: only the first CTA's range can start before the tile
             auto cta_slot = [&](int c) { return 2 * (kPair ? 2 * c + rank : c); };  // first partial slot of CTA c's rank
             const int slot0 = cta_slot(c_first) + (start2(c_first) >= T0 ? 0 : 1);
+            TTS_ASSERT(slot0 >= 0 && cta_slot(c_last) + 1 < 2 * kMaxCtas);
             auto part_of = [&](int k) { return p.partial + (size_t)(k == 0 ? slot0 : cta_slot(c_first + k)) * kPartFloats; };
             // latency-bound (L2 round trips under full HBM load): every batch of
             // loads is issued before any is consumed
