@@ -713,7 +713,9 @@ __global__ void __maxnreg__(kMaxRegs)
     // (TTS_PROF: [0] waiting for a free slot, [1] issuing, [2] item loads)
     PROF_DECL;
     const int nslot = is_k ? kNK : kNV;
-    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+    // TTS_L2HINT: 1 evict_last / evict_first, 2 evict_last / normal, 3 normal / evict_first
+    const uint64_t pol_keep = p.l2hint == 3 ? l2_policy_evict_normal() : l2_policy_evict_last();
+    const uint64_t pol_stream = p.l2hint == 2 ? l2_policy_evict_normal() : l2_policy_evict_first();
     const uint32_t b_f = is_k ? b_kfull : b_vfull, b_e = is_k ? b_kempty : b_vempty;
     int slot = 0, js = 0;
     uint32_t ph = 0;

@@ -115,7 +115,7 @@ struct Ctx {
   bool env_no_pdl = false;    // TTS_NO_PDL: no programmatic dependent launch
   bool umma_ok = false;       // tcgen05 path usable on this device (umma_prepare)
   int env_round_robin = 0;    // TTS_ROUND_ROBIN=1: beam b of a group on lane quadrant b % 4
-  int env_l2hint = 1;         // TTS_L2HINT=0: no L2 eviction priorities by cross-group sharing (k_tree_umma; measured +0.5-2 %)
+  int env_l2hint = 0;         // TTS_L2HINT=1-3: L2 eviction priorities by cross-group sharing (k_tree_umma; DRAM bytes unchanged, off)
   int env_pair = 0;           // TTS_PAIR=1: 2-CTA clusters for groups of > umma_max_beams beams (measured slower)
   int env_sched = 2;          // TTS_SCHED: phase-1 tile assignment of k_tree_umma (0 rotated, 1 round-robin, 2 none:
                               // every unit split evenly, measured fastest on C3)
