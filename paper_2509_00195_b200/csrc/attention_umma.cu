@@ -568,6 +568,21 @@ __global__ void __maxnreg__(kMaxRegs)
       run += __shfl_sync(0xffffffffu, x, 31);
     }
     if (lane == 0) s_pre[0] = 0;
+    __syncwarp();
+    // sched 4 (group-proportional stream-K, below): usable when every group
+    // with units gets >= 1 CTA and >= 1 unit per CTA
+    const int Sw = s_pre[p.n_groups];
+    const int Cw = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int ns = p.n_layers * p.Hkv;
+    bool okp = Sw > 0 && p.n_groups <= Cw;
+    for (int i = lane; okp && i < p.n_groups; i += 32) {
+      const int u = s_pre[i + 1] - s_pre[i];
+      const int c0 = (int)((2ll * Cw * s_pre[i] + Sw) / (2ll * Sw));
+      const int c1 = (int)((2ll * Cw * s_pre[i + 1] + Sw) / (2ll * Sw));
+      if (u > 0 && (c1 <= c0 || (int64_t)ns * u < c1 - c0)) okp = false;
+    }
+    okp = __all_sync(0xffffffffu, okp);
+    if (lane == 0) s_info[1] = okp;
   }
   __syncthreads();
   const int S = s_pre[p.n_groups];  // units per (layer, kv head) slab
@@ -596,7 +611,13 @@ __global__ void __maxnreg__(kMaxRegs)
   // puts the ng groups of a slab on CTAs about C / ng apart at the same
   // relative offset -- processed at the same time, so the pages they share
   // hit L2 -- with the same exact unit balance.
-  const bool gmaj = p.sched == 3;
+  // sched 4: group-major order, and each group its own block of CTAs in
+  // proportion to its units (CTA boundary of group g: C s_pre[g] / S, rounded),
+  // its units split evenly inside the block -- every group reaches slab s at
+  // the same point of the call, so the pages the groups of a slab share are
+  // fetched from HBM about once (L2), with the units still balanced
+  const bool prop = k1 == 0 && p.sched == 4 && s_info[1];
+  const bool gmaj = p.sched == 3 || prop;
   const int nslab = p.n_layers * p.Hkv;
   auto U0 = [&](int gi, int slab) -> int64_t {  // first unit of tile (slab, gi) in the sequence
     return gmaj ? (int64_t)nslab * s_pre[gi] + (int64_t)slab * (s_pre[gi + 1] - s_pre[gi]) : (int64_t)slab * S + s_pre[gi];
@@ -621,7 +642,7 @@ __global__ void __maxnreg__(kMaxRegs)
   // ~(c+1) U / C units in total, start2(c) = base2 + c U / C - (phase-1 units
   // of CTAs < c).  Otherwise an even split of the phase-2 units.
   const bool bal = k1 > 0 && U2 > 0;
-  const int C2 = bal ? Cg : (int)min((int64_t)Cg, U2);
+  const int C2 = bal || prop ? Cg : (int)min((int64_t)Cg, U2);
   auto f1 = [&](int cc) {  // phase-1 units of CTAs [0, cc)
     int64_t a = 0;
     const int cb = cc / ng * ng;  // whole blocks: the same tiles as without rotation
@@ -634,7 +655,20 @@ __global__ void __maxnreg__(kMaxRegs)
     }
     return a;
   };
-  auto start2 = [&](int cc) {
+  auto csg = [&](int g) { return (int)((2ll * Cg * s_pre[g] + S) / (2ll * S)); };  // first CTA of group g (prop)
+  auto start2 = [&](int cc) -> int64_t {
+    if (prop) {
+      if (cc >= Cg) return U;
+      int lo = -1, hi = ng - 1;  // smallest g with csg(g + 1) > cc
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (csg(mid + 1) > cc) hi = mid;
+        else lo = mid;
+      }
+      const int g = hi, c0 = csg(g), cn = csg(g + 1) - c0;
+      const int64_t wg = (int64_t)nslab * (s_pre[g + 1] - s_pre[g]);
+      return (int64_t)nslab * s_pre[g] + (int64_t)(cc - c0) * wg / cn;
+    }
     return bal ? base2 + (int64_t)cc * U / Cg - f1(cc) : base2 + (int64_t)cc * U2 / C2;
   };
   const int64_t ua2 = cta < C2 ? start2(cta) : 0;
@@ -1166,6 +1200,17 @@ __global__ void __maxnreg__(kMaxRegs)
           asm volatile("bar.sync 1, 256;" ::: "memory");
           const int64_t T0 = U0(gi, slab);
           auto cta_of = [&](int64_t x) {  // the phase-2 CTA whose range holds unit x
+            if (prop) {
+              int lo = 0, hi = ng;  // the group of unit x (largest g with nslab * s_pre[g] <= x)
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if ((int64_t)nslab * s_pre[mid] <= x) lo = mid;
+                else hi = mid;
+              }
+              const int c0 = csg(lo), cn = csg(lo + 1) - c0;
+              const int64_t wg = (int64_t)nslab * (s_pre[lo + 1] - s_pre[lo]);
+              return c0 + (int)(((x - (int64_t)nslab * s_pre[lo] + 1) * cn - 1) / wg);
+            }
             if (!bal) return (int)(((x - base2 + 1) * C2 - 1) / U2);
             int lo = 0, hi = C2;  // largest c with start2(c) <= x
             while (hi - lo > 1) {
