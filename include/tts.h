@@ -128,8 +128,8 @@ int64_t tts_launch_count(tts_ctx_t ctx);
 
 /* Name of the attention kernel this context's decode calls launch:
  * "k_tree_umma" (tcgen05, d = 128, 4 <= G <= 16, one CTA resident per SM) or
- * "k_tree_attn" (mma.sync: d = 64, G < 4, or a device where the tcgen05
- * kernel's residency does not hold). */
+ * "k_tree_attn" (mma.sync: d = 64, G < 4, or a device with more SMs than the
+ * tcgen05 kernel's split-tile partial slots cover). */
 const char* tts_attention_kernel(tts_ctx_t ctx);
 
 /* a1. Install request `req` with n_beams beams on a prompt of prompt_len

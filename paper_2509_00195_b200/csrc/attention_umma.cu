@@ -215,7 +215,7 @@ struct UInline {
 // beam's last page (V -> the pool's fp16); a fresh page's slots 1..P-1 zeroed.
 struct PlanParams {
   int32_t* lens;
-  const int32_t* refcounts;  // item.w = 1: the page is also held by beams outside the group
+  const int32_t* refcounts;  // non-null (TTS_L2HINT): item.w = 1 when the page is also held outside the group
   const int32_t* tables;
   const GroupDesc* groups;  // device copies when the call does not fit the parameter block, else null
   const int32_t* glens;
@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
       if (t >= 0) {
         if (t != last) {
           if (last >= 0)
-            out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), __ldg(p.refcounts + last) > __popc(mem));
+            out[o++] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP),
+                                 p.refcounts && __ldg(p.refcounts + last) > __popc(mem));
           last = t;
           mem = 1u << b;
           s0 = b;
@@ -383,7 +384,8 @@ __global__ void __launch_bounds__(kPlanThreads, 8) k_plan(PlanParams p, const __
         }
       }
     }
-    if (last >= 0) out[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), __ldg(p.refcounts + last) > __popc(mem));
+    if (last >= 0)
+      out[o] = make_int4(last, (int)mem, min(kP, s_len[s0] - i * kP), p.refcounts && __ldg(p.refcounts + last) > __popc(mem));
     base += tot;
     __syncthreads();
   }
@@ -1437,7 +1439,7 @@ cudaError_t launch_attention_umma(Ctx* c, const GroupDesc* groups_h, int n_group
                                   const __nv_bfloat16* v_new, cudaStream_t st, bool pair) {
   PlanParams pp;
   pp.lens = c->buf.seq_lens;
-  pp.refcounts = c->buf.refcounts;
+  pp.refcounts = c->env_l2hint ? c->buf.refcounts : nullptr;  // (only the L2 hints read item.w)
   pp.tables = c->buf.block_tables;
   pp.groups = nullptr;
   pp.glens = nullptr;
